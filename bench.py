@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""Benchmark: DPD particle-steps/s on B200 (BASELINE.json metric, config C3).
+
+One "step" = one full DPD timestep of Alg. 1 over the synthetic
+4,194,304-particle rho=3 fluid (C3): fused Verlet + signatures every step,
+reorder (keys + radix sort + permute + cell list) and ordered neighbor build
+every rebuild_every=10 steps, pair forces every step.  Inputs (state 0.7 GB,
+table 2.1 GB) are far larger than the 126 MB L2, so no explicit L2 flush.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Under torchrun each rank simulates its own 4M box (replicas: the spatial
+brick decomposition is not built yet), timed on the device with CUDA events,
+max over ranks; rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+UNIT = "M particle-steps/s"
+N_C3 = 2**22
+RHO = 3.0
+FALLBACK_HBM = 6650.0
+
+
+def c3_box():
+    L = (N_C3 / RHO) ** (1.0 / 3.0)
+    return L
+
+
+def synth_state(n, L, seed=2024, kbt=1.0):
+    """Synthetic C3 inputs (S:44-52 semantics: uniform positions, Maxwell-
+    Boltzmann velocities with zero net momentum, tags 1..N)."""
+    g = np.random.default_rng(seed)
+    x, y, z = (g.uniform(0.0, L, n) for _ in range(3))
+    for a in (x, y, z):
+        a[a >= L] = 0.0
+    v = [g.normal(0.0, np.sqrt(kbt), n) for _ in range(3)]
+    for a in v:
+        a -= a.mean()
+    tag = np.arange(1, n + 1, dtype=np.uint32)
+    return [x, y, z] + v + [tag]
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return FALLBACK_HBM, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap", "power.draw"]
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.12)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return ws, rank, local
+
+
+def barrier_sync(ws):
+    import torch
+
+    torch.cuda.synchronize()
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        torch.cuda.synchronize()
+
+
+def max_over_ranks(x, ws, local):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------- CPU arms
+def cpu_sample(state, L, max_seconds=25.0, nthreads=None):
+    """The oracle's whole-step CPU driver (Alg. 1) on the same C3 system:
+    times up to 10 consecutive steps (step 10 is a rebuild) within max_seconds."""
+    import oracle as O
+
+    nthreads = nthreads or len(os.sched_getaffinity(0))
+    obox = O.make_box((0, 0, 0), (L, L, L))
+    sim = O.Sim(obox, O.make_params(), tuple(state), nthreads=nthreads)
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < 10 and time.perf_counter() - t_start < max_seconds:
+        t0 = time.perf_counter()
+        sim.run(1)
+        times.append(time.perf_counter() - t0)
+    n = len(state[0])
+    if len(times) == 10:  # 9 plain steps + 1 rebuild step = exactly one rebuild period
+        per_step = sum(times) / 10
+        sample = f"C3 {n} particles, steps 1-10 (one rebuild period), oracle port"
+    else:
+        per_step = sum(times) / len(times)
+        sample = f"C3 {n} particles, steps 1-{len(times)} (no rebuild in sample), oracle port"
+    return n / per_step / 1e6, nthreads, sample, len(times)
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    L = c3_box()
+    state = synth_state(N_C3, L)
+    val, cores, sample, nsteps = cpu_sample(state, L, max_seconds=float(args.ref_seconds))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(val, 4), "unit": UNIT,
+        "n_gpus": args.gpus, "steps": nsteps, "warmup": 0, "ms_per_step": N_C3 / (val * 1e6) * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_dict(ws),
+        "cpu_baseline": {"value": round(val, 4), "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(val, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(ws):
+    return {"workload": "C3: homogeneous DPD fluid, 4,194,304 particles per GPU, rho=3, "
+                        "L=111.818, a=25, gamma=4.5, kT=1, rc=1, dt=0.01, skin=0.3, rebuild=10",
+            "particles_per_gpu": N_C3, "rho": RHO, "rebuild_every": 10, "max_neighbors": 128,
+            "parallelism": f"replicas{ws}" if ws > 1 else "single",
+            "l2": "inputs > L2 (0.7 GB state + 2.1 GB table vs 126 MB L2); no flush"}
+
+
+# --------------------------------------------------------------- B200 arm
+def run_b200(args, ws, rank, local):
+    import torch
+
+    import paper_1311_0402_b200 as dpd
+
+    torch.cuda.set_device(local)
+    L = c3_box()
+    state = synth_state(N_C3, L, seed=2024 + rank)
+    box = dpd.SimBox((0.0, 0.0, 0.0), (L, L, L))
+    params = dpd.PairParams()
+    run = dpd.RunConfig()
+    e = dpd.Engine(box, params, run, capacity=N_C3, device=local)
+    e.upload(dpd.ParticleStore.from_arrays(*state))
+    e.setup()
+    e.step(args.warmup)
+    barrier_sync(ws)
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        ms, stage_ms, launches = e.step_timed(args.steps, stages=True)
+        barrier_sync(ws)
+        wall = time.perf_counter() - t0
+    ms_max = max_over_ranks(ms, ws, local)
+    stats = e.table_stats()
+    nbar = stats["mean_row"]
+    total_particles = N_C3 * ws
+    value = total_particles * args.steps / (ms_max * 1e-3) / 1e6
+
+    # roofline of the dominant kernel (pair force): per particle
+    # 16 (pos|tag) + 16 (vel|sig) + 4 (counts) + 4 nbar (row) + 12 (force)
+    force_launch_ms = stage_ms[3] / max(launches[3], 1)
+    bytes_per_launch = N_C3 * (48.0 + 4.0 * nbar)
+    achieved = bytes_per_launch / (force_launch_ms * 1e-3) / 1e9
+    peak, peak_kind = peaks()
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "force_dram_bytes.json")
+    if os.path.exists(prof):
+        traffic = json.load(open(prof)).get("bytes_per_launch")
+    # full-step byte model (reported only): B = 48 + 4n + (16 + 4n)/R
+    step_bytes = N_C3 * (48.0 + 4.0 * nbar + (16.0 + 4.0 * nbar) / run.rebuild_every)
+    step_ms = ms / args.steps
+
+    # end to end through the public API with host buffers (pinned): upload,
+    # setup, K steps with the per-step thermo read-back, download
+    pinned = [torch.from_numpy(a).pin_memory().numpy() for a in state]
+    out = [torch.empty(N_C3, dtype=torch.float64).pin_memory().numpy() for _ in range(6)]
+    barrier_sync(ws)
+    t0 = time.perf_counter()
+    e.upload(dpd.ParticleStore.from_arrays(*pinned))
+    e.setup()
+    for _ in range(args.steps):
+        e.step(1)
+        e.thermo()
+    s = e.download()
+    for k in range(3):
+        out[k][:] = s.coord[k]
+        out[3 + k][:] = s.veloc[k]
+    barrier_sync(ws)
+    e2e_s = max_over_ranks(time.perf_counter() - t0, ws, local)
+    e2e = total_particles * args.steps / e2e_s / 1e6
+    h2d = N_C3 * (6 * 8 + 4)
+    d2h_state = N_C3 * (9 * 8 + 4 + 1 + 4)
+    d2h = d2h_state / args.steps + 2 * 64
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 5),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (uniform positions, Maxwell-Boltzmann velocities, seed 2024+rank)",
+        "config": config_dict(ws),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": traffic, "kernel": "k_force",
+                     "bytes_per_launch": bytes_per_launch, "mean_row": round(nbar, 3),
+                     "launch_ms": round(force_launch_ms, 5)},
+        "step_roofline": {"bytes_per_step": step_bytes,
+                          "achieved_gbs": round(step_bytes / (step_ms * 1e-3) / 1e9, 1),
+                          "frac": round(step_bytes / (step_ms * 1e-3) / 1e9 / peak, 4)},
+        "stage_ms_per_step": {k: round(stage_ms[i] / args.steps, 5) for i, k in
+                              enumerate(["integrate", "sort_permute", "build", "force", "other"])},
+        "gpu_launches": int(launches[5]),
+        "e2e": {"value": round(e2e, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d / args.steps),
+                "d2h_bytes_per_step": int(d2h),
+                "note": "upload + setup + K x (dpdb_step(1) + thermo read) + download, pinned host"},
+        "clocks": clk.summary(),
+        "wall_s_timed": round(wall, 4),
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        val, cores, sample, _ = cpu_sample(state, L, max_seconds=float(args.ref_seconds))
+        line["cpu_baseline"] = {"value": round(val, 4), "unit": UNIT, "cores": cores,
+                                "kind": "port", "sample": sample}
+    e.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-seconds", default=25.0, type=float)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    ws, rank, local = dist_init()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_b200(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

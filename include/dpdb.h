@@ -1,0 +1,192 @@
+/*
+ * dpdb.h -- C ABI of the B200-native DPD engine (libdpdb.so).
+ *
+ * This is the drop-in boundary for the reference's per-step hot path.  The
+ * reference is a C++20 library whose hot-path entry points are:
+ *
+ *   CellGrid::make                    inc/cell_grid.hpp:39-43
+ *   reorder_particles                 inc/cell_grid.hpp:78-79  (src/cell_grid.cpp:166-198)
+ *   local_cell_ranks/build_cell_list  inc/cell_grid.hpp:74,82  (src/cell_grid.cpp:136-164)
+ *   RadixSorter::sort / radix_sort    inc/radix_sort.hpp:15-27 (src/radix_sort.cpp:16-74)
+ *   build_coarse_stencil              inc/stencil.hpp:24       (src/stencil.cpp:7-41)
+ *   expand_fine_stencil               inc/stencil.hpp:39-40    (src/stencil.cpp:43-62)
+ *   build_neighbor_table              inc/neighbor_table.hpp:45-47 (impl. not shipped)
+ *   join_core_skin / tile_transpose   inc/neighbor_table.hpp:51,55
+ *   make_signature / pair_uniforms /
+ *   gaussian / fastlog / fastcos2pi /
+ *   fastpow / tea_hash                inc/rng.hpp:25-91, inc/fastmath.hpp:92-151
+ *   compute_forces / bond_forces      SPEC.md:434-451 (impl. not shipped)
+ *   verlet_step / apply_body_force    SPEC.md:488-505 (impl. not shipped)
+ *   compute_temperature               inc/core.hpp:116 (src/core.cpp:141-149)
+ *
+ * Conventions (mirroring the reference's):
+ *   - return 0 on success, otherwise the reference ErrorCategory value
+ *     (inc/error.hpp:8-13): 1 config, 2 physics, 3 protocol, 4 io; plus
+ *     5 = CUDA/device error.  dpdb_last_error() gives the message.
+ *   - host arrays are caller-owned and only touched during the call; every
+ *     call is synchronous at the boundary and runs on the context's stream.
+ *   - a context is not thread-safe (the reference's WorkerPool runs one job
+ *     at a time, src/parallel.cpp:63-83).
+ *   - there is no CPU fallback: creating a context without an sm_100 device
+ *     fails with code 5.
+ */
+#ifndef DPDB_H
+#define DPDB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DPDB_OK 0
+#define DPDB_ECONFIG 1
+#define DPDB_EPHYSICS 2
+#define DPDB_EPROTOCOL 3
+#define DPDB_EIO 4
+#define DPDB_EDEVICE 5
+
+/* SimBox, inc/core.hpp:15-25 */
+typedef struct {
+    double lo[3], hi[3];
+    int32_t periodic[3];
+    int32_t wall[3];
+} dpdb_box;
+
+/* PairParams, inc/core.hpp:51-68 (sigma derived: sigma^2 = 2 gamma kbt) */
+typedef struct {
+    int32_t n_species;          /* 1..4 */
+    double a[16], gamma[16];    /* n_species x n_species, row-major, symmetric */
+    double kbt, s, r_c, dt;
+} dpdb_params;
+
+/* RunConfig subset, inc/core.hpp:83-109 */
+typedef struct {
+    int32_t rebuild_every;      /* default 10 */
+    double skin;                /* default 0.3 */
+    double body_force;          /* double-Poiseuille g, 0 = off */
+    int32_t drive_axis;         /* default 2 */
+    int32_t partition_axis;     /* default 0 */
+    uint32_t seed;              /* default 1 */
+    uint32_t max_neighbors;     /* default 128, multiple of 32, <= 4096 */
+    int32_t sub_bits;           /* default 2 (inc/cell_grid.hpp:30) */
+} dpdb_run;
+
+/* thermo line */
+typedef struct {
+    int64_t step;
+    uint64_t n;
+    double kbt;                 /* compute_temperature, COM-subtracted */
+    double momentum[3];
+} dpdb_thermo;
+
+/* CellGrid geometry, inc/cell_grid.hpp:21-70 */
+typedef struct {
+    int32_t ncell[3], ncell_ext[3], wrapmode[3];
+    int32_t bits_per_axis, key_bits;
+    uint32_t n_local_cells, n_total_cells;
+    double cell_size[3], inv_cell[3], origin[3];
+} dpdb_grid_info;
+
+typedef struct dpdb_ctx dpdb_ctx;
+
+const char* dpdb_version(void);
+/* last error of ctx (or of the calling thread when ctx is NULL) */
+const char* dpdb_last_error(const dpdb_ctx* ctx);
+/* number of CUDA devices with compute capability 10.x, or -1 on error */
+int dpdb_device_count(void);
+
+/* ---------------------------------------------------------------- context */
+int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, const dpdb_run* run,
+                size_t capacity, dpdb_ctx** out);
+int dpdb_destroy(dpdb_ctx* ctx);
+int dpdb_grid(const dpdb_ctx* ctx, dpdb_grid_info* out);
+/* rank_of_cell[n_total_cells] (ext lattice index -> rank) */
+int dpdb_grid_ranks(const dpdb_ctx* ctx, uint32_t* rank_of_cell);
+/* CUDA stream of the context (cudaStream_t) for interop */
+void* dpdb_stream(dpdb_ctx* ctx);
+
+/* ------------------------------------------------------- state transfer */
+/* ParticleStore SoA, inc/core.hpp:29-47.  species/molecule may be NULL. */
+int dpdb_upload(dpdb_ctx* ctx, size_t n, const double* x, const double* y, const double* z,
+                const double* vx, const double* vy, const double* vz, const uint32_t* tag,
+                const uint8_t* species, const uint32_t* molecule);
+int dpdb_upload_forces(dpdb_ctx* ctx, const double* fx, const double* fy, const double* fz);
+/* any pointer may be NULL */
+int dpdb_download(dpdb_ctx* ctx, double* x, double* y, double* z, double* vx, double* vy,
+                  double* vz, double* fx, double* fy, double* fz, uint32_t* tag,
+                  uint8_t* species, uint32_t* signature);
+int dpdb_size(const dpdb_ctx* ctx, size_t* n);
+/* Harmonic bonds (BondTopology, inc/core.hpp:70-81): K (r - r0) along the bond */
+int dpdb_set_bonds(dpdb_ctx* ctx, size_t nb, const uint32_t* tag_i, const uint32_t* tag_j,
+                   const double* k, const double* r0);
+
+/* ------------------------------------------- per-stage entry points */
+/* sort keys of the current (unsorted) state, src/cell_grid.cpp:168-175 */
+int dpdb_sort_keys(dpdb_ctx* ctx, uint32_t* keys);
+/* reorder_particles: keys -> stable radix sort -> permute -> cell list.
+ * perm (old -> new, may be NULL) as returned by the reference. */
+int dpdb_reorder(dpdb_ctx* ctx, uint32_t* perm);
+int dpdb_cell_start(dpdb_ctx* ctx, uint32_t* cell_start /* n_total_cells + 1 */);
+/* coarse stencil in the reference CSR form: offsets[n_local_cells+1], cells[] */
+int dpdb_coarse_stencil(dpdb_ctx* ctx, uint32_t* offsets, uint32_t* cells);
+/* fine stencil (expand_fine_stencil): offsets[n_local_cells+1]; indices may be
+ * NULL to query the size (offsets[n_local_cells]) */
+int dpdb_fine_stencil(dpdb_ctx* ctx, uint32_t* offsets, uint32_t* indices);
+/* build_neighbor_table over the current (reordered) state */
+int dpdb_build_neighbors(dpdb_ctx* ctx);
+/* layout transforms of the device table */
+int dpdb_join_core_skin(dpdb_ctx* ctx);
+int dpdb_tile_transpose(dpdb_ctx* ctx);
+/* export: entries[n_rows_pad * max_neighbors] in the table's CURRENT layout,
+ * unused slots zeroed; core/skin counts u16 per row.  tiled and joined report
+ * the layout flags (NeighborTable::tiled/joined, inc/neighbor_table.hpp:22-23). */
+int dpdb_get_neighbors(dpdb_ctx* ctx, uint32_t* entries, uint16_t* core, uint16_t* skin,
+                       int32_t* tiled, int32_t* joined);
+/* per-particle signatures from the current fp64 velocities */
+int dpdb_signatures(dpdb_ctx* ctx, uint32_t* sig);
+/* compute_forces + bond_forces + apply_body_force with step_mix(seed, step) */
+int dpdb_compute_forces(dpdb_ctx* ctx, uint32_t step);
+int dpdb_verlet_phase1(dpdb_ctx* ctx);
+int dpdb_verlet_phase2(dpdb_ctx* ctx);
+
+/* ------------------------------------------------- device-resident path */
+/* Alg. 1 setup: reorder, cell list, build, signatures, forces(step 0) */
+int dpdb_setup(dpdb_ctx* ctx);
+/* nsteps of Alg. 1's main loop; rebuild every rebuild_every */
+int dpdb_step(dpdb_ctx* ctx, int64_t nsteps);
+int dpdb_thermo_get(dpdb_ctx* ctx, dpdb_thermo* out);
+/* Runs nsteps like dpdb_step and returns the device time (CUDA events on the
+ * context stream, ms).  stage_ms[0..5] (may be NULL): integrate, sort+permute,
+ * build, force, other, total; stage_launches[0..5] likewise (kernel launches). */
+int dpdb_step_timed(dpdb_ctx* ctx, int64_t nsteps, double* ms, double* stage_ms,
+                    int64_t* stage_launches);
+int64_t dpdb_current_step(const dpdb_ctx* ctx);
+/* mean / max row length (core + skin) of the current table; mean_core too */
+int dpdb_table_stats(dpdb_ctx* ctx, double* mean_row, double* mean_core, uint32_t* max_row);
+
+/* --------------------------------------- device primitives (parity) */
+enum {
+    DPDB_OP_TEA_HASH = 1,      /* in0,in1 u32; param = rounds; out u32[2n] */
+    DPDB_OP_SIGNATURE = 2,     /* in0 u32 tag; in1 f64[3n] v (xyz interleaved); out u32 */
+    DPDB_OP_PAIR_UNIFORMS = 3, /* in0 u32[2n] sig, in1 u32[2n] tag; param = step_mix; out u32[2n] */
+    DPDB_OP_GAUSSIAN64 = 4,    /* in0,in1 u32; out f64 */
+    DPDB_OP_GAUSSIAN32 = 5,    /* in0,in1 u32; out f32 (hot-path variant) */
+    DPDB_OP_FASTLOG = 6,       /* in0 u32; out f64 */
+    DPDB_OP_FASTCOS2PI = 7,    /* in0 u32; out f64 */
+    DPDB_OP_FASTPOW = 8,       /* in0,in1 f64; out f64 */
+    DPDB_OP_MORTON = 9,        /* in0 u32[3n]; param = bits; out u32 */
+    DPDB_OP_FASTLOG32 = 10,    /* in0 u32; out f32 */
+    DPDB_OP_STEP_MIX = 11      /* in0 u32 seed, in1 u32 step; out u32 */
+};
+int dpdb_eval(int device, int op, size_t n, const void* in0, const void* in1, uint32_t param,
+              void* out);
+/* stable LSD radix sort on the device (RadixSorter::sort contract): host
+ * arrays in/out, bit_length multiple of 4 and <= 32 */
+int dpdb_radix_sort(int device, uint32_t* keys, uint32_t* vals, size_t n, int bit_length);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -52,6 +52,11 @@ class Params(C.Structure):
                 ("dt", C.c_double)]
 
 
+class Bond(C.Structure):
+    _fields_ = [("tag_i", C.c_uint32), ("tag_j", C.c_uint32), ("k", C.c_double),
+                ("r0", C.c_double)]
+
+
 class OracleError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"[{code}] {msg}")
@@ -123,6 +128,9 @@ def _declare(L):
                                    u32p, u, u, i, i, u32p, u16p, u16p, f64p, f64p, f64p, i]),
         "orc_pair_force": (i, [C.POINTER(Params), C.c_uint8, C.c_uint8, f64p, f64p, d, f64p]),
         "orc_body_force": (None, [d, sz, f64p, d, f64p]),
+        "orc_bond_forces": (i, [C.POINTER(Box), sz, C.POINTER(Bond), sz, u32p, f64p, f64p, f64p,
+                                f64p, f64p, f64p]),
+        "orc_raw_index": (sz, [i, u, u, u]),
         "orc_verlet_phase1": (i, [C.POINTER(Box), d, sz, f64p, f64p, f64p, f64p, f64p, f64p,
                                   f64p, f64p, f64p, C.c_void_p]),
         "orc_verlet_phase2": (None, [d, sz, f64p, f64p, f64p, f64p, f64p, f64p]),

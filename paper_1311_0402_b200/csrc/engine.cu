@@ -1,0 +1,1143 @@
+// engine.cu -- host side of the B200 DPD engine: device context, Alg. 1 step
+// driver and the C ABI declared in include/dpdb.h.
+//
+// Host code is C++; every per-particle operation is a hand-written sm_100a
+// kernel (kernels.cuh).  There is no CPU fallback: without a compute
+// capability 10.x device every entry point fails with DPDB_EDEVICE.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "dpdb.h"
+#include "grid.hpp"
+#include "kernels.cuh"
+
+using dpdb::DevErr;
+using dpdb::HostGrid;
+
+namespace {
+thread_local std::string g_thread_err;
+
+constexpr int BUILD_WARPS = 4;
+constexpr int BUILD_TILES = 2;
+constexpr int FORCE_THREADS = 128;
+constexpr int RED_BLOCKS = 296;
+
+enum Stage { ST_INTEGRATE = 0, ST_SORT = 1, ST_BUILD = 2, ST_FORCE = 3, ST_OTHER = 4, ST_N = 5 };
+}  // namespace
+
+struct dpdb_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    dpdb_box box{};
+    dpdb_params params{};
+    dpdb_run run{};
+    HostGrid grid;
+    double sigma[16]{};
+    size_t cap = 0, n = 0, n_pad = 0;
+    uint32_t maxn = 128;
+    // device state
+    double *x[3]{}, *v[3]{}, *x2[3]{}, *v2[3]{};
+    float *f[3]{}, *f2[3]{};
+    uint32_t *tag{}, *tag2{}, *mol{}, *mol2{};
+    uint8_t *sp{}, *sp2{};
+    float4 *pos4{}, *vel4{};
+    uint32_t *keys{}, *keys2{}, *vals{}, *vals2{}, *hist{};
+    uint32_t *cell_start{}, *rank_of_cell{}, *stencil{};
+    uint8_t *stencil_n{}, *cell_flags{};
+    uint32_t *entries{}, *counts{};
+    DevErr* err{};
+    double *red{}, *red_out{};
+    uint32_t* tmp_u32{};
+    // bonds (CSR by tag; index_of_tag refreshed at every permute)
+    uint32_t *bond_off{}, *bond_partner{}, *index_of_tag{};
+    float *bond_k{}, *bond_r0{};
+    size_t n_bonds = 0;
+    uint32_t max_tag = 0;
+    // flags
+    bool has_mol = false, have_sorted = false, have_table = false, tiled = true, joined = false;
+    int64_t step = 0;
+    std::string last_error;
+    // stage timing
+    bool timing = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<int> ev_stage;
+    size_t ev_used = 0;
+    int64_t launches[ST_N]{};
+};
+
+namespace {
+
+int fail(dpdb_ctx* ctx, int code, const std::string& msg) {
+    if (ctx)
+        ctx->last_error = msg;
+    else
+        g_thread_err = msg;
+    return code;
+}
+
+#define CK(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(ctx, DPDB_EDEVICE, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define CKL()                                                                                 \
+    do {                                                                                      \
+        cudaError_t e_ = cudaGetLastError();                                                  \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(ctx, DPDB_EDEVICE, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define TRY(...)                    \
+    do {                            \
+        int rc_ = (__VA_ARGS__);    \
+        if (rc_) return rc_;        \
+    } while (0)
+
+inline unsigned blocks_for(size_t n, unsigned t) { return (unsigned)((n + t - 1) / t); }
+
+template <class T>
+int dalloc(dpdb_ctx* ctx, T*& p, size_t count) {
+    CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+    return 0;
+}
+
+int check_device(dpdb_ctx* ctx) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    DevErr e{};
+    CK(cudaMemcpy(&e, ctx->err, sizeof e, cudaMemcpyDeviceToHost));
+    if (!e.code) return 0;
+    CK(cudaMemset(ctx->err, 0, sizeof(DevErr)));
+    std::string msg;
+    switch (e.what) {
+        case dpdb::EW_NONFINITE:
+            msg = "blow-up: non-finite or escaped particle, tag " + std::to_string(e.tag);
+            break;
+        case dpdb::EW_MIGRATION:
+            msg = "particle outside its domain slab (missed migration), tag " + std::to_string(e.tag);
+            break;
+        case dpdb::EW_OVERFLOW:
+            msg = "neighbor table: row overflow (max_neighbors=" + std::to_string(ctx->maxn) +
+                  ", needed " + std::to_string(e.tag2) + ") for particle tag " + std::to_string(e.tag);
+            break;
+        case dpdb::EW_COINCIDENT:
+            msg = "coincident particles, tags " + std::to_string(e.tag) + " and " + std::to_string(e.tag2);
+            break;
+        case dpdb::EW_BOND:
+            msg = "bond " + std::to_string(e.tag) + "-" + std::to_string(e.tag2) + ": missing endpoint";
+            break;
+        default:
+            msg = "device error";
+    }
+    return fail(ctx, e.code, msg);
+}
+
+void mark(dpdb_ctx* ctx, int stage) {
+    if (!ctx->timing) return;
+    if (ctx->ev_used == ctx->ev_pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        ctx->ev_pool.push_back(e);
+        ctx->ev_stage.push_back(0);
+    }
+    cudaEventRecord(ctx->ev_pool[ctx->ev_used], ctx->stream);
+    ctx->ev_stage[ctx->ev_used] = stage;
+    ++ctx->ev_used;
+}
+
+dpdb::DevGrid dev_grid(const dpdb_ctx* ctx) {
+    dpdb::DevGrid g{};
+    const HostGrid& h = ctx->grid;
+    for (int k = 0; k < 3; ++k) {
+        g.slab_lo[k] = h.slab_lo[k];
+        g.slab_hi[k] = h.slab_hi[k];
+        g.inv_cell[k] = h.inv_cell[k];
+        g.origin[k] = h.origin[k];
+        g.cell_size[k] = h.cell_size[k];
+        g.centre[k] = (h.slab_lo[k] + h.slab_hi[k]) / 2;
+        g.ncell[k] = h.ncell[k];
+        g.ncell_ext[k] = h.ncell_ext[k];
+        g.ghost_lo[k] = h.ghost_lo[k];
+    }
+    g.sub_bits = h.sub_bits;
+    g.rank_of_cell = ctx->rank_of_cell;
+    return g;
+}
+
+dpdb::BoundaryArgs boundary(const dpdb_ctx* ctx) {
+    dpdb::BoundaryArgs b{};
+    for (int k = 0; k < 3; ++k) {
+        b.lo[k] = ctx->box.lo[k];
+        b.hi[k] = ctx->box.hi[k];
+        b.L[k] = ctx->box.hi[k] - ctx->box.lo[k];
+        b.periodic[k] = ctx->box.periodic[k];
+        b.wall[k] = ctx->box.wall[k];
+    }
+    return b;
+}
+
+// fp32 wrap lengths of the single-domain slab (wrapmode axes)
+void wrap_lengths(const dpdb_ctx* ctx, float L[3], float H[3]) {
+    for (int k = 0; k < 3; ++k) {
+        const double len = ctx->grid.slab_hi[k] - ctx->grid.slab_lo[k];
+        L[k] = (float)len;
+        H[k] = (float)(0.5 * len);
+    }
+}
+
+template <bool P2, bool P1, bool KEYS, bool STREAMS>
+int launch_integrate(dpdb_ctx* ctx) {
+    if (!ctx->n) return 0;
+    dpdb::IntegrateArgs a{};
+    for (int k = 0; k < 3; ++k) {
+        a.x[k] = ctx->x[k];
+        a.v[k] = ctx->v[k];
+        a.f[k] = ctx->f[k];
+    }
+    a.tag = ctx->tag;
+    a.pos4 = ctx->pos4;
+    a.vel4 = ctx->vel4;
+    a.keys = ctx->keys;
+    a.vals = ctx->vals;
+    a.err = ctx->err;
+    a.bnd = boundary(ctx);
+    a.grid = dev_grid(ctx);
+    a.dt = ctx->params.dt;
+    a.h = 0.5 * ctx->params.dt;
+    a.n = (uint32_t)ctx->n;
+    dpdb::k_integrate<P2, P1, KEYS, STREAMS><<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(a);
+    CKL();
+    ctx->launches[ST_INTEGRATE]++;
+    return 0;
+}
+
+int radix_sort_on(dpdb_ctx* ctx, cudaStream_t st, uint32_t*& k, uint32_t*& v, uint32_t*& k2,
+                  uint32_t*& v2, uint32_t* hist, size_t n, int bits) {
+    if (n == 0 || bits == 0) return 0;
+    const uint32_t tiles = (uint32_t)((n + dpdb::RS_TILE - 1) / dpdb::RS_TILE);
+    for (int shift = 0; shift < bits; shift += 8) {
+        const int width = std::min(8, bits - shift);
+        const uint32_t mask = (1u << width) - 1u;
+        dpdb::k_radix_upsweep<<<tiles, dpdb::RS_THREADS, 0, st>>>(k, (uint32_t)n, shift, mask, tiles, hist);
+        dpdb::k_scan_exclusive<<<1, 1024, 0, st>>>(hist, 256u * tiles);
+        dpdb::k_radix_downsweep<<<tiles, dpdb::RS_THREADS, 0, st>>>(k, v, k2, v2, (uint32_t)n, shift,
+                                                                    mask, tiles, hist);
+        CKL();
+        if (ctx) ctx->launches[ST_SORT] += 3;
+        std::swap(k, k2);
+        std::swap(v, v2);
+    }
+    return 0;
+}
+
+int do_sort(dpdb_ctx* ctx) {
+    return radix_sort_on(ctx, ctx->stream, ctx->keys, ctx->vals, ctx->keys2, ctx->vals2, ctx->hist,
+                         ctx->n, ctx->grid.key_bits());
+}
+
+// index_of_tag refresh for bonds
+__global__ void k_index_of_tag(const uint32_t* tag, uint32_t n, uint32_t* iot, uint32_t max_tag) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n && tag[t] <= max_tag) iot[tag[t]] = t;
+}
+
+int refresh_bond_index(dpdb_ctx* ctx) {
+    if (!ctx->n_bonds || !ctx->n) return 0;
+    CK(cudaMemsetAsync(ctx->index_of_tag, 0xFF, ((size_t)ctx->max_tag + 1) * 4, ctx->stream));
+    k_index_of_tag<<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(ctx->tag, (uint32_t)ctx->n,
+                                                                    ctx->index_of_tag, ctx->max_tag);
+    CKL();
+    ctx->launches[ST_OTHER]++;
+    return 0;
+}
+
+int do_permute(dpdb_ctx* ctx, bool forces) {
+    if (!ctx->n) {
+        CK(cudaMemsetAsync(ctx->cell_start, 0, ((size_t)ctx->grid.n_total_cells + 1) * 4, ctx->stream));
+        ctx->have_sorted = true;
+        return 0;
+    }
+    dpdb::PermuteArgs a{};
+    for (int k = 0; k < 3; ++k) {
+        a.xin[k] = ctx->x[k];
+        a.vin[k] = ctx->v[k];
+        a.xout[k] = ctx->x2[k];
+        a.vout[k] = ctx->v2[k];
+        a.fin[k] = ctx->f[k];
+        a.fout[k] = ctx->f2[k];
+        a.centre[k] = (ctx->grid.slab_lo[k] + ctx->grid.slab_hi[k]) / 2;
+    }
+    a.tag_in = ctx->tag;
+    a.tag_out = ctx->tag2;
+    a.sp_in = ctx->sp;
+    a.sp_out = ctx->sp2;
+    a.mol_in = ctx->mol;
+    a.mol_out = ctx->mol2;
+    a.order = ctx->vals;
+    a.keys = ctx->keys;
+    a.cell_start = ctx->cell_start;
+    a.pos4 = ctx->pos4;
+    a.vel4 = ctx->vel4;
+    a.n = (uint32_t)ctx->n;
+    a.n_total_cells = ctx->grid.n_total_cells;
+    a.key_shift = 3 * ctx->grid.sub_bits;
+    const unsigned nb = blocks_for(ctx->n, 256);
+    if (forces && ctx->has_mol)
+        dpdb::k_permute<true, true><<<nb, 256, 0, ctx->stream>>>(a);
+    else if (forces)
+        dpdb::k_permute<true, false><<<nb, 256, 0, ctx->stream>>>(a);
+    else if (ctx->has_mol)
+        dpdb::k_permute<false, true><<<nb, 256, 0, ctx->stream>>>(a);
+    else
+        dpdb::k_permute<false, false><<<nb, 256, 0, ctx->stream>>>(a);
+    CKL();
+    ctx->launches[ST_SORT]++;
+    for (int k = 0; k < 3; ++k) {
+        std::swap(ctx->x[k], ctx->x2[k]);
+        std::swap(ctx->v[k], ctx->v2[k]);
+        if (forces) std::swap(ctx->f[k], ctx->f2[k]);
+    }
+    std::swap(ctx->tag, ctx->tag2);
+    std::swap(ctx->sp, ctx->sp2);
+    if (ctx->has_mol) std::swap(ctx->mol, ctx->mol2);
+    ctx->have_sorted = true;
+    ctx->have_table = false;
+    return refresh_bond_index(ctx);
+}
+
+size_t build_smem(const dpdb_ctx* ctx) {
+    constexpr int P = 32 * BUILD_TILES;
+    return BUILD_WARPS * 32 * sizeof(float4) + P * 4 + (size_t)ctx->maxn * (P + 1) * 4;
+}
+
+int do_build(dpdb_ctx* ctx) {
+    if (!ctx->have_sorted) return fail(ctx, DPDB_ECONFIG, "build_neighbor_table: particles not reordered");
+    ctx->tiled = true;
+    ctx->joined = false;
+    ctx->have_table = true;
+    if (!ctx->n) return 0;
+    dpdb::BuildArgs a{};
+    a.pos4 = ctx->pos4;
+    a.keys = ctx->keys;
+    a.cell_start = ctx->cell_start;
+    a.stencil = ctx->stencil;
+    a.stencil_n = ctx->stencil_n;
+    a.cell_flags = ctx->cell_flags;
+    a.entries = ctx->entries;
+    a.counts = ctx->counts;
+    a.err = ctx->err;
+    a.n_local = (uint32_t)ctx->n;
+    a.maxn = ctx->maxn;
+    a.n_local_cells = ctx->grid.n_local_cells;
+    a.key_shift = 3 * ctx->grid.sub_bits;
+    const double rc = ctx->params.r_c, rs = ctx->params.r_c + ctx->run.skin;
+    a.cut_c = (float)(rc * rc);
+    a.cut_s = (float)(rs * rs);
+    wrap_lengths(ctx, a.L, a.H);
+    constexpr int P = 32 * BUILD_TILES;
+    const size_t smem = build_smem(ctx);
+    dpdb::k_build<BUILD_WARPS, BUILD_TILES>
+        <<<blocks_for(ctx->n, P), BUILD_WARPS * 32, smem, ctx->stream>>>(a);
+    CKL();
+    ctx->launches[ST_BUILD]++;
+    return 0;
+}
+
+int do_streams(dpdb_ctx* ctx, uint32_t* sig_out) {
+    if (!ctx->n) return 0;
+    const HostGrid& g = ctx->grid;
+    dpdb::k_streams<<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(
+        ctx->x[0], ctx->x[1], ctx->x[2], ctx->v[0], ctx->v[1], ctx->v[2], ctx->tag, ctx->pos4,
+        ctx->vel4, sig_out, (g.slab_lo[0] + g.slab_hi[0]) / 2, (g.slab_lo[1] + g.slab_hi[1]) / 2,
+        (g.slab_lo[2] + g.slab_hi[2]) / 2, (uint32_t)ctx->n);
+    CKL();
+    ctx->launches[ST_OTHER]++;
+    return 0;
+}
+
+template <int SMODE, bool TILED, bool JOINED>
+void force_launch(dpdb_ctx* ctx, const dpdb::ForceArgs& a, bool body) {
+    const unsigned nb = blocks_for(ctx->n, FORCE_THREADS);
+    if (body)
+        dpdb::k_force<SMODE, TILED, JOINED, true><<<nb, FORCE_THREADS, 0, ctx->stream>>>(a);
+    else
+        dpdb::k_force<SMODE, TILED, JOINED, false><<<nb, FORCE_THREADS, 0, ctx->stream>>>(a);
+}
+
+template <int SMODE>
+void force_dispatch_layout(dpdb_ctx* ctx, const dpdb::ForceArgs& a, bool body) {
+    if (ctx->tiled && !ctx->joined) force_launch<SMODE, true, false>(ctx, a, body);
+    else if (ctx->tiled) force_launch<SMODE, true, true>(ctx, a, body);
+    else if (!ctx->joined) force_launch<SMODE, false, false>(ctx, a, body);
+    else force_launch<SMODE, false, true>(ctx, a, body);
+}
+
+int do_forces(dpdb_ctx* ctx, uint32_t step) {
+    if (!ctx->have_table) return fail(ctx, DPDB_ECONFIG, "compute_forces: neighbor table not built");
+    if (!ctx->n) return 0;
+    const dpdb_params& p = ctx->params;
+    dpdb::ForceArgs a{};
+    a.pos4 = ctx->pos4;
+    a.vel4 = ctx->vel4;
+    a.entries = ctx->entries;
+    a.counts = ctx->counts;
+    a.xpart = ctx->x[ctx->run.partition_axis];
+    for (int k = 0; k < 3; ++k) a.f[k] = ctx->f[k];
+    a.err = ctx->err;
+    a.n = (uint32_t)ctx->n;
+    a.maxn = ctx->maxn;
+    a.step_mix = dpdb::step_mix_of(ctx->run.seed, step);
+    a.rc2 = (float)(p.r_c * p.r_c);
+    a.inv_rc = (float)(1.0 / p.r_c);
+    a.a = (float)p.a[0];
+    a.gamma = (float)p.gamma[0];
+    a.sigma_dt = (float)(ctx->sigma[0] / std::sqrt(p.dt));
+    wrap_lengths(ctx, a.L, a.H);
+    const bool body = ctx->run.body_force != 0.0;
+    a.body_g = (float)ctx->run.body_force;
+    a.drive_axis = ctx->run.drive_axis;
+    const int pa = ctx->run.partition_axis;
+    a.body_mid64 = 0.5 * (ctx->box.lo[pa] + ctx->box.hi[pa]);
+    a.s_exp = (float)p.s;
+    if (p.s == 1.0) force_dispatch_layout<1>(ctx, a, body);
+    else if (p.s == 2.0) force_dispatch_layout<2>(ctx, a, body);
+    else if (p.s == 3.0) force_dispatch_layout<3>(ctx, a, body);
+    else force_dispatch_layout<0>(ctx, a, body);
+    CKL();
+    ctx->launches[ST_FORCE]++;
+    if (ctx->n_bonds) {
+        dpdb::BondArgs b{};
+        b.boff = ctx->bond_off;
+        b.bpartner = ctx->bond_partner;
+        b.bk = ctx->bond_k;
+        b.br0 = ctx->bond_r0;
+        b.index_of_tag = ctx->index_of_tag;
+        b.pos4 = ctx->pos4;
+        for (int k = 0; k < 3; ++k) {
+            b.f[k] = ctx->f[k];
+            b.periodic[k] = ctx->box.periodic[k];
+        }
+        wrap_lengths(ctx, b.L, b.H);
+        b.err = ctx->err;
+        b.n = (uint32_t)ctx->n;
+        b.max_tag = ctx->max_tag;
+        dpdb::k_bonds<<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(b);
+        CKL();
+        ctx->launches[ST_FORCE]++;
+    }
+    return 0;
+}
+
+int do_reorder_all(dpdb_ctx* ctx, bool forces) {
+    TRY(launch_integrate<false, false, true, false>(ctx));
+    TRY(do_sort(ctx));
+    return do_permute(ctx, forces);
+}
+
+int require_ctx(const dpdb_ctx* ctx) {
+    if (!ctx) return fail(nullptr, DPDB_ECONFIG, "null context");
+    return 0;
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+const char* dpdb_version(void) { return "dpdb 0.1 (sm_100a)"; }
+
+const char* dpdb_last_error(const dpdb_ctx* ctx) {
+    return ctx ? ctx->last_error.c_str() : g_thread_err.c_str();
+}
+
+int dpdb_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return -1;
+    int ok = 0;
+    for (int d = 0; d < n; ++d) {
+        cudaDeviceProp p;
+        if (cudaGetDeviceProperties(&p, d) == cudaSuccess && p.major == 10) ++ok;
+    }
+    return ok;
+}
+
+int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, const dpdb_run* run,
+                size_t capacity, dpdb_ctx** out) {
+    dpdb_ctx* ctx = nullptr;
+    if (!out || !box || !params || !run) return fail(nullptr, DPDB_ECONFIG, "null argument");
+    *out = nullptr;
+    // validation mirrors SimBox::validate, PairParams::make, RunConfig::validate
+    for (int k = 0; k < 3; ++k) {
+        if (!(box->hi[k] > box->lo[k]))
+            return fail(nullptr, DPDB_ECONFIG, "box: hi must exceed lo on axis " + std::to_string(k));
+        if (box->periodic[k] && box->wall[k])
+            return fail(nullptr, DPDB_ECONFIG, "box: axis cannot be periodic and walled");
+    }
+    if (!(params->r_c > 0)) return fail(nullptr, DPDB_ECONFIG, "pair params: r_c must be positive");
+    if (!(params->s > 0)) return fail(nullptr, DPDB_ECONFIG, "pair params: weight exponent s must be positive");
+    if (params->n_species < 1 || params->n_species > 4)
+        return fail(nullptr, DPDB_ECONFIG, "pair params: 1..4 species supported");
+    const int ns = params->n_species;
+    for (int i = 0; i < ns; ++i)
+        for (int j = 0; j < i; ++j)
+            if (params->a[i * ns + j] != params->a[j * ns + i] ||
+                params->gamma[i * ns + j] != params->gamma[j * ns + i])
+                return fail(nullptr, DPDB_ECONFIG, "pair params: matrices must be symmetric");
+    if (ns != 1)
+        return fail(nullptr, DPDB_ECONFIG, "pair params: multi-species pair forces not yet on the device path");
+    if (run->rebuild_every < 1) return fail(nullptr, DPDB_ECONFIG, "run: rebuild interval must be >= 1");
+    if (!(run->skin >= 0)) return fail(nullptr, DPDB_ECONFIG, "run: skin distance must be >= 0");
+    if (run->max_neighbors == 0 || run->max_neighbors % 32 || run->max_neighbors > 4096)
+        return fail(nullptr, DPDB_ECONFIG, "run: max_neighbors must be a multiple of 32 in [32, 4096]");
+    if (run->drive_axis < 0 || run->drive_axis > 2 || run->partition_axis < 0 || run->partition_axis > 2)
+        return fail(nullptr, DPDB_ECONFIG, "run: axes must be 0, 1 or 2");
+    ctx = new dpdb_ctx();
+    ctx->device = device;
+    ctx->box = *box;
+    ctx->params = *params;
+    ctx->run = *run;
+    ctx->maxn = run->max_neighbors;
+    for (int q = 0; q < ns * ns; ++q) ctx->sigma[q] = std::sqrt(2.0 * params->gamma[q] * params->kbt);
+    std::string err;
+    const int dims[3] = {1, 1, 1}, crd[3] = {0, 0, 0};
+    int rc = ctx->grid.make(*box, box->lo, box->hi, dims, crd, params->r_c + run->skin,
+                            run->sub_bits, err);
+    if (rc) {
+        fail(nullptr, rc, err);
+        delete ctx;
+        return rc;
+    }
+    {
+        int ndev = 0;
+        cudaDeviceProp prop;
+        const char* why = nullptr;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+            why = "no CUDA device (the engine has no CPU fallback)";
+        else if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10)
+            why = "device is not compute capability 10.x (sm_100a build)";
+        if (why) {
+            fail(nullptr, DPDB_EDEVICE, std::string(why) + ", device " + std::to_string(device));
+            delete ctx;
+            return DPDB_EDEVICE;
+        }
+    }
+    auto bail = [&](int code) {
+        g_thread_err = ctx->last_error;
+        dpdb_destroy(ctx);
+        return code;
+    };
+    if (cudaSetDevice(device) != cudaSuccess) return bail(fail(ctx, DPDB_EDEVICE, "cudaSetDevice"));
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess)
+        return bail(fail(ctx, DPDB_EDEVICE, "cudaStreamCreate"));
+    ctx->cap = std::max<size_t>(capacity, 1);
+    ctx->n_pad = (ctx->cap + 31) & ~(size_t)31;
+    const size_t c = ctx->n_pad;
+    const HostGrid& g = ctx->grid;
+    for (int k = 0; k < 3; ++k) {
+        if ((rc = dalloc(ctx, ctx->x[k], c)) || (rc = dalloc(ctx, ctx->v[k], c)) ||
+            (rc = dalloc(ctx, ctx->x2[k], c)) || (rc = dalloc(ctx, ctx->v2[k], c)) ||
+            (rc = dalloc(ctx, ctx->f[k], c)) || (rc = dalloc(ctx, ctx->f2[k], c)))
+            return bail(rc);
+    }
+    const uint32_t tiles = (uint32_t)((c + dpdb::RS_TILE - 1) / dpdb::RS_TILE);
+    if ((rc = dalloc(ctx, ctx->tag, c)) || (rc = dalloc(ctx, ctx->tag2, c)) ||
+        (rc = dalloc(ctx, ctx->sp, c)) || (rc = dalloc(ctx, ctx->sp2, c)) ||
+        (rc = dalloc(ctx, ctx->mol, c)) || (rc = dalloc(ctx, ctx->mol2, c)) ||
+        (rc = dalloc(ctx, ctx->pos4, c)) || (rc = dalloc(ctx, ctx->vel4, c)) ||
+        (rc = dalloc(ctx, ctx->keys, c)) || (rc = dalloc(ctx, ctx->keys2, c)) ||
+        (rc = dalloc(ctx, ctx->vals, c)) || (rc = dalloc(ctx, ctx->vals2, c)) ||
+        (rc = dalloc(ctx, ctx->hist, (size_t)256 * tiles)) ||
+        (rc = dalloc(ctx, ctx->cell_start, (size_t)g.n_total_cells + 1)) ||
+        (rc = dalloc(ctx, ctx->rank_of_cell, (size_t)g.n_total_cells)) ||
+        (rc = dalloc(ctx, ctx->stencil, (size_t)g.n_local_cells * 32)) ||
+        (rc = dalloc(ctx, ctx->stencil_n, (size_t)g.n_local_cells)) ||
+        (rc = dalloc(ctx, ctx->cell_flags, (size_t)g.n_local_cells)) ||
+        (rc = dalloc(ctx, ctx->entries, c * ctx->maxn)) || (rc = dalloc(ctx, ctx->counts, c)) ||
+        (rc = dalloc(ctx, ctx->err, 1)) || (rc = dalloc(ctx, ctx->red, (size_t)RED_BLOCKS * 4)) ||
+        (rc = dalloc(ctx, ctx->red_out, 8)) || (rc = dalloc(ctx, ctx->tmp_u32, c)))
+        return bail(rc);
+    if (cudaMemset(ctx->err, 0, sizeof(DevErr)) != cudaSuccess ||
+        cudaMemset(ctx->counts, 0, c * 4) != cudaSuccess ||
+        cudaMemset(ctx->sp, 0, c) != cudaSuccess || cudaMemset(ctx->sp2, 0, c) != cudaSuccess ||
+        cudaMemset(ctx->f[0], 0, c * 4) != cudaSuccess || cudaMemset(ctx->f[1], 0, c * 4) != cudaSuccess ||
+        cudaMemset(ctx->f[2], 0, c * 4) != cudaSuccess)
+        return bail(fail(ctx, DPDB_EDEVICE, "cudaMemset"));
+    std::vector<uint32_t> rows;
+    std::vector<uint8_t> cnt, flags;
+    g.coarse_stencil(rows, cnt, flags);
+    if (cudaMemcpy(ctx->rank_of_cell, g.rank_of_cell.data(), g.rank_of_cell.size() * 4,
+                   cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(ctx->stencil, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(ctx->stencil_n, cnt.data(), cnt.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(ctx->cell_flags, flags.data(), flags.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+        return bail(fail(ctx, DPDB_EDEVICE, "upload of grid tables failed"));
+    const size_t smem = build_smem(ctx);
+    if (cudaFuncSetAttribute(dpdb::k_build<BUILD_WARPS, BUILD_TILES>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return bail(fail(ctx, DPDB_ECONFIG, "max_neighbors too large for the builder's shared memory"));
+    *out = ctx;
+    return 0;
+}
+
+int dpdb_destroy(dpdb_ctx* ctx) {
+    if (!ctx) return 0;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    void* ptrs[] = {ctx->tag, ctx->tag2, ctx->mol, ctx->mol2, ctx->sp, ctx->sp2, ctx->pos4,
+                    ctx->vel4, ctx->keys, ctx->keys2, ctx->vals, ctx->vals2, ctx->hist,
+                    ctx->cell_start, ctx->rank_of_cell, ctx->stencil, ctx->stencil_n,
+                    ctx->cell_flags, ctx->entries, ctx->counts, ctx->err, ctx->red, ctx->red_out,
+                    ctx->tmp_u32, ctx->bond_off, ctx->bond_partner, ctx->index_of_tag,
+                    ctx->bond_k, ctx->bond_r0};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    for (int k = 0; k < 3; ++k) {
+        void* q[] = {ctx->x[k], ctx->v[k], ctx->x2[k], ctx->v2[k], ctx->f[k], ctx->f2[k]};
+        for (void* p : q)
+            if (p) cudaFree(p);
+    }
+    for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return 0;
+}
+
+int dpdb_grid(const dpdb_ctx* ctx, dpdb_grid_info* o) {
+    TRY(require_ctx(ctx));
+    const HostGrid& g = ctx->grid;
+    for (int k = 0; k < 3; ++k) {
+        o->ncell[k] = g.ncell[k];
+        o->ncell_ext[k] = g.ncell_ext[k];
+        o->wrapmode[k] = g.wrap[k];
+        o->cell_size[k] = g.cell_size[k];
+        o->inv_cell[k] = g.inv_cell[k];
+        o->origin[k] = g.origin[k];
+    }
+    o->bits_per_axis = g.bits_per_axis;
+    o->key_bits = g.key_bits();
+    o->n_local_cells = g.n_local_cells;
+    o->n_total_cells = g.n_total_cells;
+    return 0;
+}
+
+int dpdb_grid_ranks(const dpdb_ctx* ctx, uint32_t* rank_of_cell) {
+    TRY(require_ctx(ctx));
+    std::memcpy(rank_of_cell, ctx->grid.rank_of_cell.data(), ctx->grid.rank_of_cell.size() * 4);
+    return 0;
+}
+
+void* dpdb_stream(dpdb_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int dpdb_upload(dpdb_ctx* ctx, size_t n, const double* x, const double* y, const double* z,
+                const double* vx, const double* vy, const double* vz, const uint32_t* tag,
+                const uint8_t* species, const uint32_t* molecule) {
+    TRY(require_ctx(ctx));
+    if (n > ctx->cap) return fail(ctx, DPDB_ECONFIG, "upload: n exceeds context capacity");
+    if (n && (!x || !y || !z || !vx || !vy || !vz || !tag))
+        return fail(ctx, DPDB_ECONFIG, "upload: null array");
+    CK(cudaSetDevice(ctx->device));
+    const double* xs[3] = {x, y, z};
+    const double* vs[3] = {vx, vy, vz};
+    for (int k = 0; k < 3; ++k) {
+        CK(cudaMemcpyAsync(ctx->x[k], xs[k], n * 8, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->v[k], vs[k], n * 8, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemsetAsync(ctx->f[k], 0, ctx->n_pad * 4, ctx->stream));
+    }
+    CK(cudaMemcpyAsync(ctx->tag, tag, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    if (species)
+        CK(cudaMemcpyAsync(ctx->sp, species, n, cudaMemcpyHostToDevice, ctx->stream));
+    else
+        CK(cudaMemsetAsync(ctx->sp, 0, ctx->n_pad, ctx->stream));
+    ctx->has_mol = molecule != nullptr;
+    if (molecule) CK(cudaMemcpyAsync(ctx->mol, molecule, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    ctx->n = n;
+    ctx->have_sorted = ctx->have_table = false;
+    ctx->step = 0;
+    TRY(refresh_bond_index(ctx));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return 0;
+}
+
+int dpdb_upload_forces(dpdb_ctx* ctx, const double* fx, const double* fy, const double* fz) {
+    TRY(require_ctx(ctx));
+    const double* fs[3] = {fx, fy, fz};
+    std::vector<float> tmp(ctx->n);
+    for (int k = 0; k < 3; ++k) {
+        for (size_t i = 0; i < ctx->n; ++i) tmp[i] = (float)fs[k][i];
+        CK(cudaMemcpy(ctx->f[k], tmp.data(), ctx->n * 4, cudaMemcpyHostToDevice));
+    }
+    return 0;
+}
+
+int dpdb_download(dpdb_ctx* ctx, double* x, double* y, double* z, double* vx, double* vy,
+                  double* vz, double* fx, double* fy, double* fz, uint32_t* tag, uint8_t* species,
+                  uint32_t* signature) {
+    TRY(require_ctx(ctx));
+    CK(cudaSetDevice(ctx->device));
+    const size_t n = ctx->n;
+    double* xs[3] = {x, y, z};
+    double* vs[3] = {vx, vy, vz};
+    double* fs[3] = {fx, fy, fz};
+    for (int k = 0; k < 3; ++k) {
+        if (xs[k]) CK(cudaMemcpyAsync(xs[k], ctx->x[k], n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        if (vs[k]) CK(cudaMemcpyAsync(vs[k], ctx->v[k], n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    if (tag) CK(cudaMemcpyAsync(tag, ctx->tag, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (species) CK(cudaMemcpyAsync(species, ctx->sp, n, cudaMemcpyDeviceToHost, ctx->stream));
+    if (signature) {
+        TRY(do_streams(ctx, ctx->tmp_u32));
+        CK(cudaMemcpyAsync(signature, ctx->tmp_u32, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    if (fx || fy || fz) {
+        std::vector<float> tmp(n);
+        for (int k = 0; k < 3; ++k) {
+            if (!fs[k]) continue;
+            CK(cudaMemcpyAsync(tmp.data(), ctx->f[k], n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+            for (size_t i = 0; i < n; ++i) fs[k][i] = tmp[i];
+        }
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    return 0;
+}
+
+int dpdb_size(const dpdb_ctx* ctx, size_t* n) {
+    TRY(require_ctx(ctx));
+    *n = ctx->n;
+    return 0;
+}
+
+int dpdb_set_bonds(dpdb_ctx* ctx, size_t nb, const uint32_t* ti, const uint32_t* tj, const double* k,
+                   const double* r0) {
+    TRY(require_ctx(ctx));
+    CK(cudaSetDevice(ctx->device));
+    // BondTopology::validate, src/core.cpp:104-114
+    uint32_t max_tag = 0;
+    std::vector<std::pair<uint32_t, uint32_t>> seen;
+    seen.reserve(nb);
+    for (size_t b = 0; b < nb; ++b) {
+        if (ti[b] == tj[b])
+            return fail(ctx, DPDB_ECONFIG, "bond topology: self bond on tag " + std::to_string(ti[b]));
+        seen.emplace_back(std::min(ti[b], tj[b]), std::max(ti[b], tj[b]));
+        max_tag = std::max(max_tag, std::max(ti[b], tj[b]));
+    }
+    std::sort(seen.begin(), seen.end());
+    for (size_t b = 1; b < seen.size(); ++b)
+        if (seen[b] == seen[b - 1])
+            return fail(ctx, DPDB_ECONFIG, "bond topology: duplicate bond " +
+                                               std::to_string(seen[b].first) + "-" +
+                                               std::to_string(seen[b].second));
+    void* old[] = {ctx->bond_off, ctx->bond_partner, ctx->index_of_tag, ctx->bond_k, ctx->bond_r0};
+    for (void* p : old)
+        if (p) cudaFree(p);
+    ctx->bond_off = ctx->bond_partner = ctx->index_of_tag = nullptr;
+    ctx->bond_k = ctx->bond_r0 = nullptr;
+    ctx->n_bonds = nb;
+    if (!nb) return 0;
+    // CSR by tag: each bond listed at both endpoints (full-list convention)
+    std::vector<uint32_t> off((size_t)max_tag + 2, 0), partner(2 * nb);
+    std::vector<float> kk(2 * nb), rr(2 * nb);
+    for (size_t b = 0; b < nb; ++b) {
+        off[ti[b] + 1]++;
+        off[tj[b] + 1]++;
+    }
+    for (size_t t = 1; t < off.size(); ++t) off[t] += off[t - 1];
+    std::vector<uint32_t> fill(off.begin(), off.end() - 1);
+    for (size_t b = 0; b < nb; ++b) {
+        uint32_t p = fill[ti[b]]++;
+        partner[p] = tj[b];
+        kk[p] = (float)k[b];
+        rr[p] = (float)r0[b];
+        p = fill[tj[b]]++;
+        partner[p] = ti[b];
+        kk[p] = (float)k[b];
+        rr[p] = (float)r0[b];
+    }
+    ctx->max_tag = max_tag;
+    int rc;
+    if ((rc = dalloc(ctx, ctx->bond_off, off.size())) || (rc = dalloc(ctx, ctx->bond_partner, 2 * nb)) ||
+        (rc = dalloc(ctx, ctx->bond_k, 2 * nb)) || (rc = dalloc(ctx, ctx->bond_r0, 2 * nb)) ||
+        (rc = dalloc(ctx, ctx->index_of_tag, (size_t)max_tag + 1)))
+        return rc;
+    CK(cudaMemcpy(ctx->bond_off, off.data(), off.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->bond_partner, partner.data(), partner.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->bond_k, kk.data(), kk.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->bond_r0, rr.data(), rr.size() * 4, cudaMemcpyHostToDevice));
+    TRY(refresh_bond_index(ctx));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return 0;
+}
+
+int dpdb_sort_keys(dpdb_ctx* ctx, uint32_t* keys) {
+    TRY(require_ctx(ctx));
+    CK(cudaSetDevice(ctx->device));
+    TRY(launch_integrate<false, false, true, false>(ctx));
+    TRY(check_device(ctx));
+    CK(cudaMemcpy(keys, ctx->keys, ctx->n * 4, cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+int dpdb_reorder(dpdb_ctx* ctx, uint32_t* perm) {
+    TRY(require_ctx(ctx));
+    CK(cudaSetDevice(ctx->device));
+    TRY(do_reorder_all(ctx, true));
+    TRY(check_device(ctx));
+    if (perm && ctx->n) {
+        std::vector<uint32_t> order(ctx->n);
+        CK(cudaMemcpy(order.data(), ctx->vals, ctx->n * 4, cudaMemcpyDeviceToHost));
+        for (size_t t = 0; t < ctx->n; ++t) perm[order[t]] = (uint32_t)t;
+    }
+    return 0;
+}
+
+int dpdb_cell_start(dpdb_ctx* ctx, uint32_t* cs) {
+    TRY(require_ctx(ctx));
+    if (!ctx->have_sorted) return fail(ctx, DPDB_ECONFIG, "cell list: particles not reordered");
+    CK(cudaMemcpy(cs, ctx->cell_start, ((size_t)ctx->grid.n_total_cells + 1) * 4, cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+int dpdb_coarse_stencil(dpdb_ctx* ctx, uint32_t* offsets, uint32_t* cells) {
+    TRY(require_ctx(ctx));
+    std::vector<uint32_t> rows;
+    std::vector<uint8_t> cnt, flags;
+    ctx->grid.coarse_stencil(rows, cnt, flags);
+    offsets[0] = 0;
+    for (uint32_t r = 0; r < ctx->grid.n_local_cells; ++r) {
+        if (cells) std::memcpy(cells + offsets[r], rows.data() + (size_t)r * 32, cnt[r] * 4);
+        offsets[r + 1] = offsets[r] + cnt[r];
+    }
+    return 0;
+}
+
+int dpdb_fine_stencil(dpdb_ctx* ctx, uint32_t* foff, uint32_t* fidx) {
+    TRY(require_ctx(ctx));
+    if (!ctx->have_sorted) return fail(ctx, DPDB_ECONFIG, "fine stencil: particles not reordered");
+    const HostGrid& g = ctx->grid;
+    std::vector<uint32_t> cs((size_t)g.n_total_cells + 1), coff(g.n_local_cells + 1);
+    CK(cudaMemcpy(cs.data(), ctx->cell_start, cs.size() * 4, cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> rows;
+    std::vector<uint8_t> cnt, flags;
+    g.coarse_stencil(rows, cnt, flags);
+    foff[0] = 0;
+    for (uint32_t r = 0; r < g.n_local_cells; ++r) {
+        uint32_t w = foff[r];
+        for (uint32_t a = 0; a < cnt[r]; ++a) {
+            const uint32_t c = rows[(size_t)r * 32 + a];
+            if (fidx)
+                for (uint32_t j = cs[c]; j < cs[c + 1]; ++j) fidx[w++] = j;
+            else
+                w += cs[c + 1] - cs[c];
+        }
+        foff[r + 1] = w;
+    }
+    return 0;
+}
+
+int dpdb_build_neighbors(dpdb_ctx* ctx) {
+    TRY(require_ctx(ctx));
+    CK(cudaSetDevice(ctx->device));
+    TRY(do_streams(ctx, nullptr));
+    TRY(do_build(ctx));
+    return check_device(ctx);
+}
+
+int dpdb_join_core_skin(dpdb_ctx* ctx) {
+    TRY(require_ctx(ctx));
+    if (!ctx->have_table) return fail(ctx, DPDB_ECONFIG, "join_core_skin: no table");
+    if (ctx->joined) return 0;
+    if (ctx->n) {
+        dpdb::k_join<<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(ctx->entries, ctx->counts,
+                                                                      (uint32_t)ctx->n, ctx->maxn,
+                                                                      ctx->tiled);
+        CKL();
+    }
+    ctx->joined = true;
+    return check_device(ctx);
+}
+
+int dpdb_tile_transpose(dpdb_ctx* ctx) {
+    TRY(require_ctx(ctx));
+    if (!ctx->have_table) return fail(ctx, DPDB_ECONFIG, "tile_transpose: no table");
+    const uint32_t rows = (uint32_t)((ctx->n + 31) & ~(size_t)31);
+    if (rows) {
+        dim3 grid(ctx->maxn / 32, rows / 32), blk(32, 8);
+        dpdb::k_tile_transpose<<<grid, blk, 0, ctx->stream>>>(ctx->entries, rows, ctx->maxn);
+        CKL();
+    }
+    ctx->tiled = !ctx->tiled;
+    return check_device(ctx);
+}
+
+int dpdb_get_neighbors(dpdb_ctx* ctx, uint32_t* entries, uint16_t* core, uint16_t* skin,
+                       int32_t* tiled, int32_t* joined) {
+    TRY(require_ctx(ctx));
+    if (!ctx->have_table) return fail(ctx, DPDB_ECONFIG, "get_neighbors: no table");
+    const size_t n = ctx->n, rows = (n + 31) & ~(size_t)31, maxn = ctx->maxn;
+    std::vector<uint32_t> cnt(n);
+    CK(cudaMemcpy(cnt.data(), ctx->counts, n * 4, cudaMemcpyDeviceToHost));
+    if (entries && rows) {
+        std::vector<uint32_t> raw(rows * maxn);
+        CK(cudaMemcpy(raw.data(), ctx->entries, raw.size() * 4, cudaMemcpyDeviceToHost));
+        std::memset(entries, 0, rows * maxn * 4);
+        auto idx = [&](uint32_t i, uint32_t k) -> size_t {
+            return ctx->tiled ? (size_t)((i & ~31u) + (k & 31u)) * maxn + (k & ~31u) + (i & 31u)
+                              : (size_t)i * maxn + k;
+        };
+        for (uint32_t i = 0; i < n; ++i) {
+            const uint32_t nc = cnt[i] & 0x1FFFu, ns = (cnt[i] >> 13) & 0x1FFFu;
+            for (uint32_t k = 0; k < nc; ++k) entries[idx(i, k)] = raw[idx(i, k)];
+            for (uint32_t s = 0; s < ns; ++s) {
+                const uint32_t k = ctx->joined ? nc + s : (uint32_t)(maxn - 1 - s);
+                entries[idx(i, k)] = raw[idx(i, k)];
+            }
+        }
+    }
+    for (size_t i = 0; i < n; ++i) {
+        if (core) core[i] = (uint16_t)(cnt[i] & 0x1FFFu);
+        if (skin) skin[i] = (uint16_t)((cnt[i] >> 13) & 0x1FFFu);
+    }
+    if (tiled) *tiled = ctx->tiled;
+    if (joined) *joined = ctx->joined;
+    return 0;
+}
+
+int dpdb_signatures(dpdb_ctx* ctx, uint32_t* sig) {
+    TRY(require_ctx(ctx));
+    CK(cudaSetDevice(ctx->device));
+    TRY(do_streams(ctx, ctx->tmp_u32));
+    CK(cudaMemcpyAsync(sig, ctx->tmp_u32, ctx->n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    return check_device(ctx);
+}
+
+int dpdb_compute_forces(dpdb_ctx* ctx, uint32_t step) {
+    TRY(require_ctx(ctx));
+    CK(cudaSetDevice(ctx->device));
+    TRY(do_streams(ctx, nullptr));
+    TRY(do_forces(ctx, step));
+    return check_device(ctx);
+}
+
+int dpdb_verlet_phase1(dpdb_ctx* ctx) {
+    TRY(require_ctx(ctx));
+    CK(cudaSetDevice(ctx->device));
+    TRY((launch_integrate<false, true, false, false>(ctx)));
+    return check_device(ctx);
+}
+
+int dpdb_verlet_phase2(dpdb_ctx* ctx) {
+    TRY(require_ctx(ctx));
+    CK(cudaSetDevice(ctx->device));
+    TRY((launch_integrate<true, false, false, false>(ctx)));
+    return check_device(ctx);
+}
+
+int dpdb_setup(dpdb_ctx* ctx) {
+    TRY(require_ctx(ctx));
+    CK(cudaSetDevice(ctx->device));
+    ctx->step = 0;
+    TRY(do_reorder_all(ctx, false));
+    TRY(do_build(ctx));
+    TRY(do_forces(ctx, 0));
+    return check_device(ctx);
+}
+
+namespace {
+int run_steps(dpdb_ctx* ctx, int64_t nsteps) {
+    if (!ctx->have_table) return fail(ctx, DPDB_ECONFIG, "step: call dpdb_setup first");
+    for (int64_t s = 0; s < nsteps; ++s) {
+        ctx->step += 1;
+        const bool rebuild = ctx->step % ctx->run.rebuild_every == 0;
+        mark(ctx, ST_OTHER);
+        if (rebuild) {
+            if (s > 0) TRY((launch_integrate<true, true, true, false>(ctx)));
+            else TRY((launch_integrate<false, true, true, false>(ctx)));
+            mark(ctx, ST_INTEGRATE);
+            TRY(do_sort(ctx));
+            TRY(do_permute(ctx, false));
+            mark(ctx, ST_SORT);
+            TRY(do_build(ctx));
+            mark(ctx, ST_BUILD);
+        } else {
+            if (s > 0) TRY((launch_integrate<true, true, false, true>(ctx)));
+            else TRY((launch_integrate<false, true, false, true>(ctx)));
+            mark(ctx, ST_INTEGRATE);
+        }
+        TRY(do_forces(ctx, (uint32_t)ctx->step));
+        mark(ctx, ST_FORCE);
+    }
+    if (nsteps > 0) {
+        TRY((launch_integrate<true, false, false, false>(ctx)));
+        mark(ctx, ST_INTEGRATE);
+    }
+    return 0;
+}
+}  // namespace
+
+int dpdb_step(dpdb_ctx* ctx, int64_t nsteps) {
+    TRY(require_ctx(ctx));
+    CK(cudaSetDevice(ctx->device));
+    TRY(run_steps(ctx, nsteps));
+    return check_device(ctx);
+}
+
+int dpdb_step_timed(dpdb_ctx* ctx, int64_t nsteps, double* ms, double* stage_ms,
+                    int64_t* stage_launches) {
+    TRY(require_ctx(ctx));
+    CK(cudaSetDevice(ctx->device));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    for (int s = 0; s < ST_N; ++s) ctx->launches[s] = 0;
+    ctx->timing = stage_ms != nullptr;
+    ctx->ev_used = 0;
+    CK(cudaEventRecord(e0, ctx->stream));
+    int rc = run_steps(ctx, nsteps);
+    cudaEventRecord(e1, ctx->stream);
+    ctx->timing = false;
+    if (rc) return rc;
+    TRY(check_device(ctx));
+    float total = 0;
+    CK(cudaEventElapsedTime(&total, e0, e1));
+    if (ms) *ms = total;
+    if (stage_ms) {
+        for (int s = 0; s <= ST_N; ++s) stage_ms[s] = 0;
+        cudaEvent_t prev = e0;
+        for (size_t q = 0; q < ctx->ev_used; ++q) {
+            float d = 0;
+            cudaEventElapsedTime(&d, prev, ctx->ev_pool[q]);
+            stage_ms[ctx->ev_stage[q]] += d;
+            prev = ctx->ev_pool[q];
+        }
+        stage_ms[ST_N] = total;
+    }
+    if (stage_launches) {
+        int64_t tot = 0;
+        for (int s = 0; s < ST_N; ++s) {
+            stage_launches[s] = ctx->launches[s];
+            tot += ctx->launches[s];
+        }
+        stage_launches[ST_N] = tot;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return 0;
+}
+
+int64_t dpdb_current_step(const dpdb_ctx* ctx) { return ctx ? ctx->step : -1; }
+
+int dpdb_table_stats(dpdb_ctx* ctx, double* mean_row, double* mean_core, uint32_t* max_row) {
+    TRY(require_ctx(ctx));
+    if (!ctx->have_table) return fail(ctx, DPDB_ECONFIG, "table_stats: no table");
+    std::vector<uint32_t> cnt(ctx->n);
+    CK(cudaMemcpy(cnt.data(), ctx->counts, ctx->n * 4, cudaMemcpyDeviceToHost));
+    double s = 0, sc = 0;
+    uint32_t mx = 0;
+    for (uint32_t c : cnt) {
+        const uint32_t nc = c & 0x1FFFu, ns = (c >> 13) & 0x1FFFu;
+        s += nc + ns;
+        sc += nc;
+        mx = std::max(mx, nc + ns);
+    }
+    const double inv = ctx->n ? 1.0 / (double)ctx->n : 0.0;
+    if (mean_row) *mean_row = s * inv;
+    if (mean_core) *mean_core = sc * inv;
+    if (max_row) *max_row = mx;
+    return 0;
+}
+
+int dpdb_thermo_get(dpdb_ctx* ctx, dpdb_thermo* out) {
+    TRY(require_ctx(ctx));
+    CK(cudaSetDevice(ctx->device));
+    out->step = ctx->step;
+    out->n = ctx->n;
+    if (!ctx->n) return fail(ctx, DPDB_EPHYSICS, "temperature of an empty system");
+    dpdb::k_sum3<<<RED_BLOCKS, 256, 0, ctx->stream>>>(ctx->v[0], ctx->v[1], ctx->v[2], nullptr,
+                                                      (uint32_t)ctx->n, ctx->red);
+    dpdb::k_sum_partials<<<1, 32, 0, ctx->stream>>>(ctx->red, RED_BLOCKS, ctx->red_out);
+    dpdb::k_mean_from_sum<<<1, 32, 0, ctx->stream>>>(ctx->red_out, 1.0 / (double)ctx->n);
+    double sums[8];
+    CK(cudaMemcpyAsync(sums, ctx->red_out, sizeof sums, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    dpdb::k_sum3<<<RED_BLOCKS, 256, 0, ctx->stream>>>(ctx->v[0], ctx->v[1], ctx->v[2],
+                                                      ctx->red_out + 4, (uint32_t)ctx->n, ctx->red);
+    dpdb::k_sum_partials<<<1, 32, 0, ctx->stream>>>(ctx->red, RED_BLOCKS, ctx->red_out);
+    double s2[8];
+    CK(cudaMemcpyAsync(s2, ctx->red_out, sizeof s2, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int k = 0; k < 3; ++k) out->momentum[k] = sums[k];
+    out->kbt = s2[3] / (3.0 * (double)ctx->n);
+    return 0;
+}
+
+int dpdb_eval(int device, int op, size_t n, const void* in0, const void* in1, uint32_t param,
+              void* out) {
+    dpdb_ctx* ctx = nullptr;
+    size_t s0 = 4, s1 = 4, so = 4;
+    switch (op) {
+        case DPDB_OP_TEA_HASH: so = 8; break;
+        case DPDB_OP_SIGNATURE: s1 = 24; break;
+        case DPDB_OP_PAIR_UNIFORMS: s0 = 8; s1 = 8; so = 8; break;
+        case DPDB_OP_GAUSSIAN64: so = 8; break;
+        case DPDB_OP_GAUSSIAN32: break;
+        case DPDB_OP_FASTLOG: s1 = 0; so = 8; break;
+        case DPDB_OP_FASTCOS2PI: s1 = 0; so = 8; break;
+        case DPDB_OP_FASTPOW: s0 = 8; s1 = 8; so = 8; break;
+        case DPDB_OP_MORTON: s0 = 12; s1 = 0; break;
+        case DPDB_OP_FASTLOG32: s1 = 0; break;
+        case DPDB_OP_STEP_MIX: break;
+        default: return fail(nullptr, DPDB_ECONFIG, "eval: unknown op");
+    }
+    if (!n) return 0;
+    CK(cudaSetDevice(device));
+    void *d0 = nullptr, *d1 = nullptr, *dout = nullptr;
+    CK(cudaMalloc(&d0, n * s0));
+    if (s1) CK(cudaMalloc(&d1, n * s1));
+    CK(cudaMalloc(&dout, n * so));
+    CK(cudaMemcpy(d0, in0, n * s0, cudaMemcpyHostToDevice));
+    if (s1) CK(cudaMemcpy(d1, in1, n * s1, cudaMemcpyHostToDevice));
+    dpdb::k_eval<<<blocks_for(n, 256), 256>>>(op, (uint32_t)n, d0, d1, param, dout);
+    CKL();
+    CK(cudaMemcpy(out, dout, n * so, cudaMemcpyDeviceToHost));
+    cudaFree(d0);
+    if (d1) cudaFree(d1);
+    cudaFree(dout);
+    return 0;
+}
+
+int dpdb_radix_sort(int device, uint32_t* keys, uint32_t* vals, size_t n, int bit_length) {
+    dpdb_ctx* ctx = nullptr;
+    if (bit_length < 0 || bit_length > 32 || bit_length % 4 != 0)
+        return fail(nullptr, DPDB_ECONFIG, "radix sort: bit length must be a multiple of 4, <= 32");
+    if (n == 0 || bit_length == 0) return 0;
+    CK(cudaSetDevice(device));
+    const uint32_t tiles = (uint32_t)((n + dpdb::RS_TILE - 1) / dpdb::RS_TILE);
+    uint32_t *k = nullptr, *v = nullptr, *k2 = nullptr, *v2 = nullptr, *h = nullptr;
+    CK(cudaMalloc(&k, n * 4));
+    CK(cudaMalloc(&v, n * 4));
+    CK(cudaMalloc(&k2, n * 4));
+    CK(cudaMalloc(&v2, n * 4));
+    CK(cudaMalloc(&h, (size_t)256 * tiles * 4));
+    CK(cudaMemcpy(k, keys, n * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(v, vals, n * 4, cudaMemcpyHostToDevice));
+    int rc = radix_sort_on(nullptr, 0, k, v, k2, v2, h, n, bit_length);
+    if (!rc) {
+        CK(cudaMemcpy(keys, k, n * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(vals, v, n * 4, cudaMemcpyDeviceToHost));
+    }
+    cudaFree(k);
+    cudaFree(v);
+    cudaFree(k2);
+    cudaFree(v2);
+    cudaFree(h);
+    return rc;
+}
+
+}  // extern "C"

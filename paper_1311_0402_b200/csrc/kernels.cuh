@@ -1,0 +1,815 @@
+// kernels.cuh -- sm_100a kernels of the B200 DPD engine.
+//
+// Data layout in HBM (one domain, n particles, n_pad = n rounded up to 32):
+//   x[3], v[3]          fp64 SoA master state (ParticleStore, inc/core.hpp:29-47)
+//   f[3]                fp32 SoA forces (accumulated in fp32)
+//   tag u32, species u8, molecule u32
+//   pos4 float4         (x - slab_centre as fp32 | tag bits)   P:234 precision model
+//   vel4 float4         (v as fp32 | signature bits)
+//   keys/vals u32       radix sort ping-pong; sorted keys double as cell ranks
+//   cell_start u32      [n_total_cells + 1]
+//   stencil u32         [n_local_cells][32] coarse stencil ranks (<=27 used)
+//   entries u32         [n_pad][maxn] neighbor table, 32x32 tile-transposed,
+//                       core from the front, skin reversed from the back
+//                       (inc/neighbor_table.hpp:12-31)
+//   counts u32          core | skin << 13 | force-wrap-flags << 26
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "dpd_math.cuh"
+
+namespace dpdb {
+
+struct DevErr {
+    int code;       // first error category seen (atomicCAS from 0)
+    uint32_t tag;   // offending particle tag
+    uint32_t tag2;  // second tag (pair errors)
+    int what;       // kernel-specific detail code
+};
+
+enum ErrWhat : int {
+    EW_NONFINITE = 1,
+    EW_ESCAPED = 2,
+    EW_MIGRATION = 3,
+    EW_OVERFLOW = 4,
+    EW_COINCIDENT = 5,
+    EW_BOND = 6,
+};
+
+__device__ __forceinline__ void raise_err(DevErr* e, int code, int what, uint32_t t1, uint32_t t2) {
+    if (atomicCAS(&e->code, 0, code) == 0) {
+        e->what = what;
+        e->tag = t1;
+        e->tag2 = t2;
+    }
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// ------------------------------------------------------------ geometry
+struct DevGrid {
+    double slab_lo[3], slab_hi[3], inv_cell[3], origin[3], cell_size[3], centre[3];
+    int ncell[3], ncell_ext[3], ghost_lo[3];
+    int sub_bits;
+    const uint32_t* rank_of_cell;
+};
+
+// src/cell_grid.cpp:97-128 + inc/cell_grid.hpp:66-68, bit-exact (no fma)
+__device__ __forceinline__ bool sort_key_of(const DevGrid& g, double x, double y, double z,
+                                            uint32_t& key) {
+    const double p[3] = {x, y, z};
+    int c[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        if (!(p[k] >= g.slab_lo[k] && p[k] < g.slab_hi[k])) return false;
+        int ci = __double2int_rd(__dmul_rn(__dsub_rn(p[k], g.slab_lo[k]), g.inv_cell[k]));
+        ci = min(max(ci, 0), g.ncell[k] - 1);
+        c[k] = ci + g.ghost_lo[k];
+    }
+    const uint32_t rank =
+        g.rank_of_cell[((size_t)c[2] * g.ncell_ext[1] + c[1]) * g.ncell_ext[0] + c[0]];
+    const int nsub = 1 << g.sub_bits;
+    uint32_t s[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double cell_lo = __dadd_rn(g.origin[k], __dmul_rn((double)c[k], g.cell_size[k]));
+        int si = __double2int_rd(
+            __dmul_rn(__dmul_rn(__dsub_rn(p[k], cell_lo), g.inv_cell[k]), (double)nsub));
+        s[k] = (uint32_t)min(max(si, 0), nsub - 1);
+    }
+    uint32_t sub = 0;
+    for (int b = 0; b < g.sub_bits; ++b)
+        sub |= (((s[0] >> b) & 1u) << (3 * b)) | (((s[1] >> b) & 1u) << (3 * b + 1)) |
+               (((s[2] >> b) & 1u) << (3 * b + 2));
+    key = (rank << (3 * g.sub_bits)) | sub;
+    return true;
+}
+
+// --------------------------------------------------------- integrator
+struct BoundaryArgs {
+    double lo[3], hi[3], L[3];
+    int periodic[3], wall[3];
+};
+
+// periodic wrap right after the position update, specular
+// walls; returns false if the particle is still outside (escaped)
+__device__ __forceinline__ bool apply_boundary(const BoundaryArgs& b, int k, double& x, double& v) {
+    if (b.periodic[k]) {
+        if (x < b.lo[k]) {
+            x = __dadd_rn(x, b.L[k]);
+            if (x >= b.hi[k]) x = b.lo[k];
+        } else if (x >= b.hi[k]) {
+            x = __dsub_rn(x, b.L[k]);
+            if (x < b.lo[k]) x = b.lo[k];
+        }
+        return x >= b.lo[k] && x < b.hi[k];
+    }
+    if (b.wall[k]) {
+        if (x >= b.hi[k]) {
+            x = __dsub_rn(__dmul_rn(2.0, b.hi[k]), x);
+            v = -v;
+            if (x >= b.hi[k]) x = nextafter(b.hi[k], b.lo[k]);
+        } else if (x < b.lo[k]) {
+            x = __dsub_rn(__dmul_rn(2.0, b.lo[k]), x);
+            v = -v;
+            if (x >= b.hi[k]) x = nextafter(b.hi[k], b.lo[k]);
+        }
+        return x >= b.lo[k] && x < b.hi[k];
+    }
+    return true;
+}
+
+struct IntegrateArgs {
+    double* x[3];
+    double* v[3];
+    const float* f[3];
+    const uint32_t* tag;
+    float4* pos4;
+    float4* vel4;
+    uint32_t* keys;
+    uint32_t* vals;
+    DevErr* err;
+    BoundaryArgs bnd;
+    DevGrid grid;
+    double dt, h;
+    uint32_t n;
+};
+
+// Fused Verlet: [phase 2 of the previous step] + phase 1 of this step +
+// boundary + either the sort keys (rebuild step; the permute kernel then
+// writes the fp32 streams) or the fp32 force streams with signatures.
+// Each half kick is its own rounding so the fp64 trajectory equals the
+// reference's phase2-then-phase1 sequence bit for bit.
+template <bool PHASE2, bool PHASE1, bool KEYS, bool STREAMS>
+__global__ void __launch_bounds__(256) k_integrate(IntegrateArgs a) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    double xs[3], vs[3];
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        double v = a.v[k][i];
+        if (PHASE2 || PHASE1) {
+            const double f = (double)a.f[k][i];
+            if (PHASE2) v = __dadd_rn(v, __dmul_rn(a.h, f));
+            if (PHASE1) v = __dadd_rn(v, __dmul_rn(a.h, f));
+        }
+        double x = a.x[k][i];
+        if (PHASE1) {
+            x = __dadd_rn(x, __dmul_rn(a.dt, v));
+            if (!(isfinite(x) && isfinite(v)))
+                ok = false;
+            else if (!apply_boundary(a.bnd, k, x, v))
+                ok = false;
+            a.x[k][i] = x;
+        }
+        if (PHASE2 || PHASE1) a.v[k][i] = v;
+        xs[k] = x;
+        vs[k] = v;
+    }
+    const uint32_t tag = (STREAMS || !ok) ? a.tag[i] : 0u;
+    if (!ok) raise_err(a.err, DPDB_EPHYSICS, EW_NONFINITE, tag, 0);
+    if (KEYS) {
+        uint32_t key = 0xFFFFFFFFu;
+        if (!sort_key_of(a.grid, xs[0], xs[1], xs[2], key))
+            raise_err(a.err, DPDB_EPROTOCOL, EW_MIGRATION, a.tag[i], 0);
+        a.keys[i] = key;
+        a.vals[i] = i;
+    }
+    if (STREAMS) {
+        const uint32_t sig = make_signature(tag, vs[0], vs[1], vs[2]);
+        a.pos4[i] = make_float4((float)(xs[0] - a.grid.centre[0]), (float)(xs[1] - a.grid.centre[1]),
+                                (float)(xs[2] - a.grid.centre[2]), __uint_as_float(tag));
+        a.vel4[i] = make_float4((float)vs[0], (float)vs[1], (float)vs[2], __uint_as_float(sig));
+    }
+}
+
+// ------------------------------------------------------- radix sort
+// Stable LSD radix sort (the RadixSorter::sort contract, inc/radix_sort.hpp:11-27;
+// paper Alg. 2) with 8-bit digits: per pass an upsweep digit
+// histogram per 4096-key tile, one exclusive scan in digit-major order, and a
+// downsweep whose in-tile ranks come from warp match/ballot -- stable by
+// construction (tile order, then round, then warp, then lane).
+constexpr int RS_THREADS = 256;
+constexpr int RS_ITEMS = 16;
+constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
+
+__global__ void __launch_bounds__(RS_THREADS) k_radix_upsweep(const uint32_t* __restrict__ keys,
+                                                              uint32_t n, int shift, uint32_t mask,
+                                                              uint32_t num_tiles,
+                                                              uint32_t* __restrict__ hist) {
+    __shared__ uint32_t h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t tile = blockIdx.x;
+    const uint32_t lane = threadIdx.x & 31;
+#pragma unroll 4
+    for (int r = 0; r < RS_ITEMS; ++r) {
+        const uint32_t idx = tile * RS_TILE + r * RS_THREADS + threadIdx.x;
+        const bool valid = idx < n;
+        const uint32_t d = valid ? (keys[idx] >> shift) & mask : 256u + lane;
+        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
+        if (valid && (__ffs(peers) - 1) == (int)lane) atomicAdd(&h[d], (uint32_t)__popc(peers));
+    }
+    __syncthreads();
+    hist[threadIdx.x * num_tiles + tile] = h[threadIdx.x];
+}
+
+// exclusive scan of m entries in place, one block of 1024 threads
+__global__ void __launch_bounds__(1024) k_scan_exclusive(uint32_t* __restrict__ data, uint32_t m) {
+    __shared__ uint32_t warp_sums[32];
+    const uint32_t t = threadIdx.x;
+    const uint32_t per = (m + 1023) / 1024;
+    const uint32_t b = min(t * per, m), e = min(b + per, m);
+    uint32_t s = 0;
+    for (uint32_t q = b; q < e; ++q) s += data[q];
+    // block exclusive scan of s
+    uint32_t incl = s;
+    const uint32_t lane = t & 31, w = t >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= (uint32_t)o) incl += y;
+    }
+    if (lane == 31) warp_sums[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t ws = warp_sums[lane];
+        uint32_t wi = ws;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+            if (lane >= (uint32_t)o) wi += y;
+        }
+        warp_sums[lane] = wi - ws;
+    }
+    __syncthreads();
+    uint32_t run = warp_sums[w] + incl - s;
+    for (uint32_t q = b; q < e; ++q) {
+        const uint32_t c = data[q];
+        data[q] = run;
+        run += c;
+    }
+}
+
+__global__ void __launch_bounds__(RS_THREADS) k_radix_downsweep(
+    const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
+    uint32_t* __restrict__ vout, uint32_t n, int shift, uint32_t mask, uint32_t num_tiles,
+    const uint32_t* __restrict__ offs) {
+    __shared__ uint32_t s_base[256];
+    __shared__ uint32_t s_cnt[8][256];
+    __shared__ uint32_t s_pref[8][256];
+    const uint32_t tile = blockIdx.x;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    s_base[threadIdx.x] = offs[threadIdx.x * num_tiles + tile];
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s_cnt[w][threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t lt = lanemask_lt();
+    for (int r = 0; r < RS_ITEMS; ++r) {
+        const uint32_t idx = tile * RS_TILE + r * RS_THREADS + threadIdx.x;
+        const bool valid = idx < n;
+        uint32_t key = 0, val = 0, d = 256u + lane;
+        if (valid) {
+            key = kin[idx];
+            val = vin[idx];
+            d = (key >> shift) & mask;
+        }
+        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
+        const uint32_t rank = __popc(peers & lt);
+        if (valid && (__ffs(peers) - 1) == (int)lane) s_cnt[warp][d] = __popc(peers);
+        __syncthreads();
+        {
+            uint32_t run = s_base[threadIdx.x];
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+                const uint32_t c = s_cnt[w][threadIdx.x];
+                s_pref[w][threadIdx.x] = run;
+                s_cnt[w][threadIdx.x] = 0;
+                run += c;
+            }
+            s_base[threadIdx.x] = run;
+        }
+        __syncthreads();
+        if (valid) {
+            const uint32_t dst = s_pref[warp][d] + rank;
+            kout[dst] = key;
+            vout[dst] = val;
+        }
+    }
+}
+
+// ------------------------------------------------ permute + cell list
+struct PermuteArgs {
+    const double* xin[3];
+    const double* vin[3];
+    double* xout[3];
+    double* vout[3];
+    const float* fin[3];
+    float* fout[3];
+    const uint32_t* tag_in;
+    uint32_t* tag_out;
+    const uint8_t* sp_in;
+    uint8_t* sp_out;
+    const uint32_t* mol_in;
+    uint32_t* mol_out;
+    const uint32_t* order;       // sorted vals: order[to] = from
+    const uint32_t* keys;        // sorted keys
+    uint32_t* cell_start;        // [n_total_cells + 1]
+    float4* pos4;
+    float4* vel4;
+    double centre[3];
+    uint32_t n, n_total_cells;
+    int key_shift;               // 3 * sub_bits
+};
+
+// reorder_particles' gather (src/cell_grid.cpp:180-195) fused with the
+// cell-boundary detection of build_cell_list (src/cell_grid.cpp:136-155) and
+// the fp32 stream + signature pack for the force/neighbor kernels.
+template <bool FORCES, bool MOL>
+__global__ void __launch_bounds__(256) k_permute(PermuteArgs a) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= a.n) return;
+    const uint32_t from = a.order[t];
+    double xs[3], vs[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        xs[k] = a.xin[k][from];
+        vs[k] = a.vin[k][from];
+        a.xout[k][t] = xs[k];
+        a.vout[k][t] = vs[k];
+        if (FORCES) a.fout[k][t] = a.fin[k][from];
+    }
+    const uint32_t tag = a.tag_in[from];
+    a.tag_out[t] = tag;
+    a.sp_out[t] = a.sp_in[from];
+    if (MOL) a.mol_out[t] = a.mol_in[from];
+    const uint32_t sig = make_signature(tag, vs[0], vs[1], vs[2]);
+    a.pos4[t] = make_float4((float)(xs[0] - a.centre[0]), (float)(xs[1] - a.centre[1]),
+                            (float)(xs[2] - a.centre[2]), __uint_as_float(tag));
+    a.vel4[t] = make_float4((float)vs[0], (float)vs[1], (float)vs[2], __uint_as_float(sig));
+    // cell_start[c] = first t with rank >= c
+    const uint32_t rmax = a.n_total_cells - 1u;  // clamp: a bad key already raised an error
+    const uint32_t r = min(a.keys[t] >> a.key_shift, rmax);
+    const uint32_t c0 = t == 0 ? 0u : min(a.keys[t - 1] >> a.key_shift, rmax) + 1u;
+    for (uint32_t c = c0; c <= r; ++c) a.cell_start[c] = t;
+    if (t == a.n - 1)
+        for (uint32_t c = r + 1; c <= a.n_total_cells; ++c) a.cell_start[c] = a.n;
+}
+
+// fp32 streams + signatures from the current fp64 state (no reorder)
+__global__ void __launch_bounds__(256) k_streams(const double* __restrict__ x0,
+                                                 const double* __restrict__ x1,
+                                                 const double* __restrict__ x2,
+                                                 const double* __restrict__ v0,
+                                                 const double* __restrict__ v1,
+                                                 const double* __restrict__ v2,
+                                                 const uint32_t* __restrict__ tag, float4* pos4,
+                                                 float4* vel4, uint32_t* sig_out, double c0,
+                                                 double c1, double c2, uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double vx = v0[i], vy = v1[i], vz = v2[i];
+    const uint32_t t = tag[i];
+    const uint32_t sig = make_signature(t, vx, vy, vz);
+    pos4[i] = make_float4((float)(x0[i] - c0), (float)(x1[i] - c1), (float)(x2[i] - c2),
+                          __uint_as_float(t));
+    vel4[i] = make_float4((float)vx, (float)vy, (float)vz, __uint_as_float(sig));
+    if (sig_out) sig_out[i] = sig;
+}
+
+// ------------------------------------------------- neighbor builder
+struct BuildArgs {
+    const float4* pos4;
+    const uint32_t* keys;        // sorted keys (rank = key >> key_shift)
+    const uint32_t* cell_start;
+    const uint32_t* stencil;     // [n_local_cells][32]
+    const uint8_t* stencil_n;
+    const uint8_t* cell_flags;
+    uint32_t* entries;
+    uint32_t* counts;
+    DevErr* err;
+    uint32_t n_local, maxn, n_local_cells;
+    int key_shift;
+    float cut_c, cut_s;
+    float L[3], H[3];
+};
+
+// fp32 minimum image, src/core.cpp:129-139 semantics with L, L/2 in fp32
+__device__ __forceinline__ float min_image_f(float d, float L, float H) {
+    if (d >= H)
+        d = __fsub_rn(d, L);
+    else if (d < -H)
+        d = __fadd_rn(d, L);
+    return d;
+}
+
+// Atomics-free ordered builder (Alg. 3).  One CTA owns P = 32*TILES
+// consecutive particles (TILES 32-row tiles of the table); its warps take the
+// cells overlapping that range round-robin.  For each cell: the fine stencil is
+// never materialized -- each lane locates its candidate k through a shuffle
+// binary search over the <=27 stencil-cell prefix sums (P:170's fine stencil
+// implicitly), so 32 candidates from several cells share one chunk.  For every
+// i of the cell: ballot(core hit) / ballot(skin hit); the insertion point is
+// the row count + popc(ballot & lanemask_lt) -- deterministic, ordered, no
+// atomics.  Rows are staged in shared memory and written out already
+// tile-transposed, so the paper's separate join/transpose passes vanish.
+template <int WARPS, int TILES>
+__global__ void __launch_bounds__(WARPS * 32) k_build(BuildArgs a) {
+    constexpr int P = 32 * TILES;
+    constexpr int STRIDE = P + 1;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float4* slots = reinterpret_cast<float4*>(smem_raw);
+    uint32_t* cnt_s = reinterpret_cast<uint32_t*>(slots + WARPS * 32);
+    uint32_t* buf = cnt_s + P;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t i0 = blockIdx.x * P;
+    if (i0 >= a.n_local) return;
+    const uint32_t iend = min(i0 + (uint32_t)P, a.n_local);
+    for (int t = threadIdx.x; t < P; t += WARPS * 32) cnt_s[t] = 0;
+    __syncthreads();
+    const uint32_t lt = lanemask_lt();
+    const uint32_t rl = a.n_local_cells - 1u;  // clamp: a bad key already raised an error
+    const uint32_t r0 = min(a.keys[i0] >> a.key_shift, rl);
+    const uint32_t r1 = min(a.keys[iend - 1] >> a.key_shift, rl);
+    const uint32_t maxn = a.maxn;
+    for (uint32_t r = r0 + warp; r <= r1; r += WARPS) {
+        const uint32_t ca = max(a.cell_start[r], i0), cb = min(a.cell_start[r + 1], iend);
+        if (ca >= cb) continue;
+        const uint32_t ns = a.stencil_n[r];
+        uint32_t sstart = 0, scount = 0;
+        if ((uint32_t)lane < ns) {
+            const uint32_t sc = a.stencil[(size_t)r * 32 + lane];
+            sstart = a.cell_start[sc];
+            scount = a.cell_start[sc + 1] - sstart;
+        }
+        uint32_t incl = scount;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t excl = incl - scount;
+        const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        const uint32_t fl = a.cell_flags[r] & 7u;
+        for (uint32_t ba = ca; ba < cb; ba += 32) {
+            const uint32_t nb = min(32u, cb - ba);
+            if ((uint32_t)lane < nb) slots[warp * 32 + lane] = a.pos4[ba + lane];
+            uint32_t mycnt = 0;  // lane l: core | skin << 16 of particle ba + l
+            __syncwarp();
+            for (uint32_t base = 0; base < total; base += 32) {
+                const uint32_t k = base + lane;
+                const bool valid = k < total;
+                int s = 0;
+#pragma unroll
+                for (int st = 16; st >= 1; st >>= 1) {
+                    const uint32_t v = __shfl_sync(0xFFFFFFFFu, incl, s + st - 1);
+                    if (v <= k) s += st;
+                }
+                const uint32_t j = __shfl_sync(0xFFFFFFFFu, sstart, s) + k -
+                                   __shfl_sync(0xFFFFFFFFu, excl, s);
+                float4 pj = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (valid) pj = __ldg(a.pos4 + j);
+                for (uint32_t ii = 0; ii < nb; ++ii) {
+                    const float4 pi = slots[warp * 32 + ii];
+                    const uint32_t i = ba + ii;
+                    float dx = __fsub_rn(pi.x, pj.x);
+                    float dy = __fsub_rn(pi.y, pj.y);
+                    float dz = __fsub_rn(pi.z, pj.z);
+                    if (fl) {
+                        if (fl & 1u) dx = min_image_f(dx, a.L[0], a.H[0]);
+                        if (fl & 2u) dy = min_image_f(dy, a.L[1], a.H[1]);
+                        if (fl & 4u) dz = min_image_f(dz, a.L[2], a.H[2]);
+                    }
+                    const float d2 =
+                        __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
+                    const bool cand = valid && j != i;
+                    const bool hc = cand && d2 <= a.cut_c;
+                    const bool hs = cand && !hc && d2 <= a.cut_s;
+                    const uint32_t mc = __ballot_sync(0xFFFFFFFFu, hc);
+                    const uint32_t ms = __ballot_sync(0xFFFFFFFFu, hs);
+                    const uint32_t c = __shfl_sync(0xFFFFFFFFu, mycnt, ii);
+                    const uint32_t col = i - i0;
+                    if (hc) {
+                        const uint32_t kp = (c & 0xFFFFu) + __popc(mc & lt);
+                        if (kp < maxn) buf[kp * STRIDE + col] = j;
+                    }
+                    if (hs) {
+                        const uint32_t sp = (c >> 16) + __popc(ms & lt);
+                        if (sp < maxn) buf[(maxn - 1 - sp) * STRIDE + col] = j;
+                    }
+                    if ((uint32_t)lane == ii) mycnt = c + __popc(mc) + ((uint32_t)__popc(ms) << 16);
+                }
+            }
+            if ((uint32_t)lane < nb) cnt_s[ba - i0 + lane] = mycnt;
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    // write-out, one 32-row tile per warp: tile-transposed raw_index layout
+    for (int tt = warp; tt < TILES; tt += WARPS) {
+        const uint32_t ti0 = i0 + 32u * tt;
+        if (ti0 >= iend) break;
+        const uint32_t col = 32u * tt + lane;
+        const uint32_t i = ti0 + lane;
+        const bool row = i < iend;
+        const uint32_t c = row ? cnt_s[col] : 0u;
+        const uint32_t nc = c & 0xFFFFu, nsk = c >> 16;
+        if (row && nc + nsk > maxn)
+            raise_err(a.err, DPDB_EPHYSICS, EW_OVERFLOW, __float_as_uint(a.pos4[i].w), nc + nsk);
+        const uint32_t maxc = __reduce_max_sync(0xFFFFFFFFu, min(nc, maxn));
+        const uint32_t maxs = __reduce_max_sync(0xFFFFFFFFu, min(nsk, maxn));
+        uint32_t* tb = a.entries + (size_t)ti0 * maxn + lane;
+        for (uint32_t k = 0; k < maxc; ++k)
+            tb[(k & 31u) * maxn + (k & ~31u)] = k < nc ? buf[k * STRIDE + col] : 0u;
+        for (uint32_t s = 0; s < maxs; ++s) {
+            const uint32_t k = maxn - 1 - s;
+            tb[(k & 31u) * maxn + (k & ~31u)] = s < nsk ? buf[k * STRIDE + col] : 0u;
+        }
+        if (row) {
+            const uint32_t ff = (a.cell_flags[min(a.keys[i] >> a.key_shift, rl)] >> 3) & 7u;
+            a.counts[i] = min(nc, 8191u) | (min(nsk, 8191u) << 13) | (ff << 26);
+        }
+    }
+}
+
+// layout transforms of the table
+__device__ __forceinline__ size_t raw_index(bool tiled, uint32_t maxn, uint32_t i, uint32_t k) {
+    return tiled ? (size_t)((i & ~31u) + (k & 31u)) * maxn + (k & ~31u) + (i & 31u)
+                 : (size_t)i * maxn + k;
+}
+
+__global__ void k_join(uint32_t* entries, const uint32_t* counts, uint32_t n, uint32_t maxn,
+                       bool tiled) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t c = counts[i], nc = c & 0x1FFFu, ns = (c >> 13) & 0x1FFFu;
+    // skin entries sit at maxn-1-s; the joined slot nc+s < maxn-1-s until they meet
+    for (uint32_t s = 0; s < ns; ++s) {
+        const uint32_t from = maxn - 1 - s, to = nc + s;
+        if (to >= from) break;
+        // swap keeps the not-yet-moved tail intact
+        const size_t pf = raw_index(tiled, maxn, i, from), pt = raw_index(tiled, maxn, i, to);
+        const uint32_t tmp = entries[pt];
+        entries[pt] = entries[pf];
+        entries[pf] = tmp;
+    }
+}
+
+// in-place 32x32 tile transpose; one CTA (32x8 threads) per tile
+__global__ void k_tile_transpose(uint32_t* entries, uint32_t n_rows_pad, uint32_t maxn) {
+    __shared__ uint32_t t[32][33];
+    const uint32_t tr = blockIdx.y * 32, tc = blockIdx.x * 32;
+    for (int y = threadIdx.y; y < 32; y += 8)
+        t[y][threadIdx.x] = entries[(size_t)(tr + y) * maxn + tc + threadIdx.x];
+    __syncthreads();
+    for (int y = threadIdx.y; y < 32; y += 8)
+        entries[(size_t)(tr + y) * maxn + tc + threadIdx.x] = t[threadIdx.x][y];
+}
+
+// ---------------------------------------------------------- forces
+struct ForceArgs {
+    const float4* pos4;
+    const float4* vel4;
+    const uint32_t* entries;
+    const uint32_t* counts;
+    const double* xpart;   // fp64 coordinate on the partition axis (body force)
+    float* f[3];
+    DevErr* err;
+    uint32_t n, maxn;
+    uint32_t step_mix;
+    float rc2, inv_rc;
+    float a, gamma, sigma_dt;  // single species: a, gamma, sigma / sqrt(dt)
+    float L[3], H[3];
+    float body_g, body_mid;
+    int drive_axis;
+    double body_mid64;
+    float s_exp;
+};
+
+__device__ __forceinline__ float weight_pow_f(float w, float s, int mode) {
+    if (mode == 1) return w;
+    if (mode == 2) return w * w;
+    if (mode == 3) return w * w * w;
+    return w > 0.f ? exp2f(s * __log2f(w)) : 0.f;
+}
+
+// Full-row pair force: thread per particle i, row
+// entries read coalesced from the tile-transposed table (core front, skin
+// back), per-step |r| <= r_c re-check, TEA-4 pair uniforms from the tag-ordered
+// signatures (inc/rng.hpp:77-83), fp32 Box-Muller, C+D+R assembled in fp32 and
+// accumulated in row order (deterministic, no atomics).
+template <int SMODE, bool TILED, bool JOINED, bool BODY>
+__global__ void __launch_bounds__(128) k_force(ForceArgs a) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    const float4 pi = a.pos4[i];
+    const float4 vi = a.vel4[i];
+    const uint32_t c = a.counts[i];
+    const uint32_t nc = c & 0x1FFFu, ns = (c >> 13) & 0x1FFFu, fl = c >> 26;
+    const uint32_t tag_i = __float_as_uint(pi.w), sig_i = __float_as_uint(vi.w);
+    const uint32_t maxn = a.maxn;
+    float fx = 0.f, fy = 0.f, fz = 0.f;
+    const uint32_t tot = nc + ns;
+    for (uint32_t m = 0; m < tot; ++m) {
+        const uint32_t k = (m < nc || JOINED) ? m : maxn - 1 - (m - nc);
+        const uint32_t j = __ldg(a.entries + raw_index(TILED, maxn, i, k));
+        const float4 pj = __ldg(a.pos4 + j);
+        float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
+        if (fl) {
+            if (fl & 1u) dx = min_image_f(dx, a.L[0], a.H[0]);
+            if (fl & 2u) dy = min_image_f(dy, a.L[1], a.H[1]);
+            if (fl & 4u) dz = min_image_f(dz, a.L[2], a.H[2]);
+        }
+        const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+        if (r2 > a.rc2) continue;
+        const float4 vj = __ldg(a.vel4 + j);
+        const uint32_t tag_j = __float_as_uint(pj.w), sig_j = __float_as_uint(vj.w);
+        if (r2 == 0.f) {
+            raise_err(a.err, DPDB_EPHYSICS, EW_COINCIDENT, tag_i, tag_j);
+            continue;
+        }
+        uint32_t u0 = tag_i < tag_j ? sig_i : sig_j;
+        uint32_t u1 = (tag_i < tag_j ? sig_j : sig_i) ^ a.step_mix;
+        tea4(u0, u1);
+        const float xi = gaussian32(u0, u1);
+        const float rinv = rsqrtf(r2);
+        const float r = r2 * rinv;
+        const float w = fmaxf(1.f - r * a.inv_rc, 0.f);
+        const float wr = weight_pow_f(w, a.s_exp, SMODE);
+        const float ex = dx * rinv, ey = dy * rinv, ez = dz * rinv;
+        const float ev = ex * (vi.x - vj.x) + ey * (vi.y - vj.y) + ez * (vi.z - vj.z);
+        const float mag = a.a * w - a.gamma * (wr * wr) * ev + a.sigma_dt * wr * xi;
+        fx = fmaf(mag, ex, fx);
+        fy = fmaf(mag, ey, fy);
+        fz = fmaf(mag, ez, fz);
+    }
+    if (BODY) {
+        const float g = a.xpart[i] < a.body_mid64 ? a.body_g : -a.body_g;
+        if (a.drive_axis == 0) fx += g;
+        else if (a.drive_axis == 1) fy += g;
+        else fz += g;
+    }
+    a.f[0][i] = fx;
+    a.f[1][i] = fy;
+    a.f[2][i] = fz;
+}
+
+// Harmonic bonds: F = -K (r - r0) e on each endpoint.  Bonds are
+// stored as a static CSR over TAGS (each bond at both endpoints), resolved
+// to current indices through index_of_tag (refreshed at every reorder), and
+// evaluated per particle -- deterministic, no atomics, like the full pair list.
+struct BondArgs {
+    const uint32_t* boff;       // [max_tag + 2]
+    const uint32_t* bpartner;   // partner tag
+    const float* bk;
+    const float* br0;
+    const uint32_t* index_of_tag;
+    const float4* pos4;
+    float* f[3];
+    DevErr* err;
+    float L[3], H[3];
+    int periodic[3];
+    uint32_t n, max_tag;
+};
+
+__global__ void k_bonds(BondArgs a) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    const float4 pi = a.pos4[i];
+    const uint32_t tag = __float_as_uint(pi.w);
+    if (tag > a.max_tag) return;
+    const uint32_t b0 = a.boff[tag], b1 = a.boff[tag + 1];
+    if (b0 == b1) return;
+    float fx = 0.f, fy = 0.f, fz = 0.f;
+    for (uint32_t b = b0; b < b1; ++b) {
+        const uint32_t pt = a.bpartner[b];
+        const uint32_t j = a.index_of_tag[pt];
+        if (j >= a.n) {
+            raise_err(a.err, DPDB_EPHYSICS, EW_BOND, tag, pt);
+            continue;
+        }
+        const float4 pj = a.pos4[j];
+        float d[3] = {pi.x - pj.x, pi.y - pj.y, pi.z - pj.z};
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            if (a.periodic[k]) d[k] = min_image_f(d[k], a.L[k], a.H[k]);
+        const float r = sqrtf(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+        const float cc = r > 0.f ? -a.bk[b] * (r - a.br0[b]) / r : 0.f;
+        fx += cc * d[0];
+        fy += cc * d[1];
+        fz += cc * d[2];
+    }
+    a.f[0][i] += fx;
+    a.f[1][i] += fy;
+    a.f[2][i] += fz;
+}
+
+// --------------------------------------------------- observables
+// deterministic two-level reductions (fixed tree, fixed partial order)
+__global__ void __launch_bounds__(256) k_sum3(const double* __restrict__ a0,
+                                              const double* __restrict__ a1,
+                                              const double* __restrict__ a2, const double* mean,
+                                              uint32_t n, double* partial) {
+    __shared__ double s[4][256];
+    double acc[4] = {0, 0, 0, 0};
+    const double m0 = mean ? mean[0] : 0.0, m1 = mean ? mean[1] : 0.0, m2 = mean ? mean[2] : 0.0;
+    for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
+        const double x = a0[i], y = a1[i], z = a2[i];
+        acc[0] += x;
+        acc[1] += y;
+        acc[2] += z;
+        const double dx = x - m0, dy = y - m1, dz = z - m2;
+        acc[3] += dx * dx + dy * dy + dz * dz;
+    }
+    for (int q = 0; q < 4; ++q) s[q][threadIdx.x] = acc[q];
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < (unsigned)o)
+            for (int q = 0; q < 4; ++q) s[q][threadIdx.x] += s[q][threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x < 4) partial[blockIdx.x * 4 + threadIdx.x] = s[threadIdx.x][0];
+}
+
+__global__ void k_sum_partials(const double* partial, int nblocks, double* out) {
+    if (threadIdx.x != 0) return;
+    double acc[4] = {0, 0, 0, 0};
+    for (int b = 0; b < nblocks; ++b)
+        for (int q = 0; q < 4; ++q) acc[q] += partial[b * 4 + q];
+    for (int q = 0; q < 4; ++q) out[q] = acc[q];
+}
+
+__global__ void k_mean_from_sum(double* sum, double inv_n) {
+    if (threadIdx.x < 3) sum[4 + threadIdx.x] = sum[threadIdx.x] * inv_n;
+}
+
+// ------------------------------------------------ parity primitives
+__global__ void k_eval(int op, uint32_t n, const void* in0, const void* in1, uint32_t param,
+                       void* out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t* u0 = static_cast<const uint32_t*>(in0);
+    const uint32_t* u1 = static_cast<const uint32_t*>(in1);
+    switch (op) {
+        case DPDB_OP_TEA_HASH: {
+            uint32_t a = u0[i], b = u1[i];
+            tea_rounds((int)param, a, b);
+            static_cast<uint32_t*>(out)[2 * i] = a;
+            static_cast<uint32_t*>(out)[2 * i + 1] = b;
+        } break;
+        case DPDB_OP_SIGNATURE: {
+            const double* v = static_cast<const double*>(in1);
+            static_cast<uint32_t*>(out)[i] = make_signature(u0[i], v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+        } break;
+        case DPDB_OP_PAIR_UNIFORMS: {
+            const uint32_t si = u0[2 * i], sj = u0[2 * i + 1];
+            const uint32_t ti = u1[2 * i], tj = u1[2 * i + 1];
+            uint32_t a = ti < tj ? si : sj, b = (ti < tj ? sj : si) ^ param;
+            tea4(a, b);
+            static_cast<uint32_t*>(out)[2 * i] = a;
+            static_cast<uint32_t*>(out)[2 * i + 1] = b;
+        } break;
+        case DPDB_OP_GAUSSIAN64:
+            static_cast<double*>(out)[i] = gaussian64(u0[i], u1[i]);
+            break;
+        case DPDB_OP_GAUSSIAN32:
+            static_cast<float*>(out)[i] = gaussian32(u0[i], u1[i]);
+            break;
+        case DPDB_OP_FASTLOG:
+            static_cast<double*>(out)[i] = fastlog64(u0[i]);
+            break;
+        case DPDB_OP_FASTCOS2PI:
+            static_cast<double*>(out)[i] = fastcos2pi64(u0[i]);
+            break;
+        case DPDB_OP_FASTPOW: {
+            const double* d0 = static_cast<const double*>(in0);
+            const double* d1 = static_cast<const double*>(in1);
+            static_cast<double*>(out)[i] = fastpow64(d0[i], d1[i]);
+        } break;
+        case DPDB_OP_MORTON: {
+            const uint32_t x = u0[3 * i], y = u0[3 * i + 1], z = u0[3 * i + 2];
+            uint32_t c = 0;
+            for (uint32_t b = 0; b < param; ++b)
+                c |= (((x >> b) & 1u) << (3 * b)) | (((y >> b) & 1u) << (3 * b + 1)) |
+                     (((z >> b) & 1u) << (3 * b + 2));
+            static_cast<uint32_t*>(out)[i] = c;
+        } break;
+        case DPDB_OP_FASTLOG32:
+            static_cast<float*>(out)[i] = fastlog32(u0[i]);
+            break;
+        case DPDB_OP_STEP_MIX:
+            static_cast<uint32_t*>(out)[i] = step_mix_of(u0[i], u1[i]);
+            break;
+        default:
+            break;
+    }
+}
+
+}  // namespace dpdb

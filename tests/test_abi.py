@@ -1,0 +1,78 @@
+"""The C-ABI boundary: libdpdb.so loads, exports every symbol include/dpdb.h
+declares, carries sm_100a code only, and refuses to run without a B200 (no
+CPU fallback).  No compute calls here -- this runs on the CPU box.
+"""
+import ctypes as C
+import os
+import re
+import shutil
+import subprocess
+
+import pytest
+
+import paper_1311_0402_b200 as dpd
+from paper_1311_0402_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "dpdb.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(dpdb_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    L = _lib.lib()
+    names = header_functions()
+    assert len(names) >= 30
+    for name in names:
+        assert hasattr(L, name), name
+    assert set(names) == set(_lib.SYMBOLS), set(names) ^ set(_lib.SYMBOLS)
+    assert L.dpdb_version().decode().startswith("dpdb")
+
+
+def test_shim_header_compiles():
+    """include/dpd_b200.hpp (C++ shim mirroring the reference API) compiles."""
+    gxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else shutil.which("g++")
+    if gxx is None:
+        pytest.skip("no g++")
+    src = os.path.join(ROOT, "include", "dpd_b200.hpp")
+    if not os.path.exists(src):
+        pytest.skip("shim header not present")
+    r = subprocess.run([gxx, "-std=c++20", "-fsyntax-only", "-x", "c++", "-I",
+                        os.path.join(ROOT, "include"), src], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+
+
+def test_sm100a_only():
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump missing")
+    out = subprocess.run([tool, "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    arches = set(re.findall(r"sm_(\d+a?)", out))
+    assert arches == {"100a"}, arches
+
+
+def test_no_cpu_fallback_without_gpu():
+    if dpd.device_count() > 0:
+        pytest.skip("a B200 is present; the no-GPU refusal is tested on CPU boxes")
+    with pytest.raises(dpd.DPDError) as e:
+        dpd.Engine(dpd.SimBox(hi=(8, 8, 8)), dpd.PairParams(), dpd.RunConfig(), capacity=10)
+    assert e.value.code == 5
+
+
+def test_config_errors_before_device():
+    """Configuration is validated like the reference (config = 1) before any device work."""
+    with pytest.raises(dpd.DPDError) as e:
+        dpd.Engine(dpd.SimBox(hi=(8, 8, 8)), dpd.PairParams(r_c=-1.0), dpd.RunConfig())
+    assert e.value.code == 1
+    with pytest.raises(dpd.DPDError) as e:
+        dpd.Engine(dpd.SimBox(hi=(8, 8, 8)), dpd.PairParams(), dpd.RunConfig(max_neighbors=100))
+    assert e.value.code == 1
+    with pytest.raises(dpd.DPDError) as e:
+        dpd.Engine(dpd.SimBox(hi=(8, 0.5, 8)), dpd.PairParams(), dpd.RunConfig())
+    assert e.value.code == 1
+    with pytest.raises(dpd.DPDError) as e:
+        dpd.radix_sort(*(__import__("numpy").zeros(4, "uint32") for _ in range(2)), 6)
+    assert e.value.code == 1

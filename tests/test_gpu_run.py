@@ -1,0 +1,113 @@
+"""Integrator parity (bit-exact fp64 Verlet) and whole-step runs of
+Alg. 1 against the oracle's CPU driver (statistical agreement)."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1311_0402_b200 as dpd
+import dpdsys as _sys
+
+pytestmark = pytest.mark.gpu
+
+
+def f32_forces(n, seed):
+    return [np.random.default_rng(seed + k).normal(size=n).astype(np.float32).astype(np.float64) * 20
+            for k in range(3)]
+
+
+@pytest.mark.parametrize("per,wall", [((1, 1, 1), (0, 0, 0)), ((0, 1, 1), (1, 0, 0))])
+def test_verlet_bitexact(per, wall):
+    box, obox, st = _sys.fluid((8, 8, 8), 3.0, per, seed=3, wall=wall)
+    n = len(st[0])
+    st = [a.copy() for a in st]
+    # push a few particles across the boundaries
+    st[0][:20] = 8.0 - 1e-4
+    st[3][:20] = 3.0
+    st[0][20:40] = 1e-4
+    st[3][20:40] = -3.0
+    F = f32_forces(n, 1)
+    e = _sys.engine(box, st)
+    e.upload_forces(*F)
+    e.verlet_phase1()
+    e.verlet_phase2()
+    s = e.download()
+    x, y, z, vx, vy, vz = [a.copy() for a in st[:6]]
+    O.check(O.lib().orc_verlet_phase1(obox, 0.01, n, x, y, z, vx, vy, vz, *F, None))
+    O.lib().orc_verlet_phase2(0.01, n, vx, vy, vz, *F)
+    for got, ref in zip(s.coord + s.veloc, [x, y, z, vx, vy, vz]):
+        assert np.array_equal(got, ref)
+    assert (s.coord[0] >= 0).all() and (s.coord[0] < 8).all()
+
+
+def test_blowup_is_physics_error():
+    box, obox, st = _sys.fluid((8, 8, 8), 3.0, seed=3)
+    st = [a.copy() for a in st]
+    st[3][7] = np.inf
+    e = _sys.engine(box, st)
+    with pytest.raises(dpd.DPDError) as ex:
+        e.verlet_phase1()
+    assert ex.value.code == 2
+
+
+def test_short_trajectory_vs_oracle():
+    """setup + 20 steps (two rebuilds) on the device vs the oracle's Alg. 1 driver."""
+    box, obox, st = _sys.fluid((12, 12, 12), 3.0, seed=21)
+    p = dpd.PairParams()
+    e = _sys.engine(box, st)
+    e.setup()
+    e.step(20)
+    assert e.current_step == 20
+    s = e.download()
+    sim = O.Sim(obox, _sys.oparams(p), st, nthreads=8)
+    sim.run(20)
+    r = sim.state()
+    og = np.argsort(s.tag)
+    orr = np.argsort(r["tag"])
+    L = 12.0
+    for k, key in enumerate("xyz"):
+        d = s.coord[k][og] - r[key][orr]
+        d -= L * np.round(d / L)
+        assert np.abs(d).max() < 1e-5, (key, np.abs(d).max())
+    for k, key in enumerate(["vx", "vy", "vz"]):
+        assert np.abs(s.veloc[k][og] - r[key][orr]).max() < 1e-3
+    th = e.thermo()
+    assert th["kbt"] == pytest.approx(sim.temperature(), rel=1e-4)
+
+
+def test_thermostat_c1():
+    """C1: 98,304 particles, rho=3: k_B T within 2% of target."""
+    box, obox, st = _sys.fluid((32, 32, 32), 3.0, seed=1)
+    e = _sys.engine(box, st)
+    e.setup()
+    e.step(300)
+    T = []
+    for _ in range(20):
+        e.step(25)
+        th = e.thermo()
+        T.append(th["kbt"])
+        assert max(abs(m) for m in th["momentum"]) < 1e-6 * len(st[0])
+    assert abs(np.mean(T) - 1.0) < 0.02
+
+
+def test_c3_properties_4m():
+    """C3 size (4,194,304 particles): size-independent properties of the table
+    and forces after a rebuild -- symmetric ascending rows, zero net force."""
+    L = (2**22 / 3.0) ** (1 / 3)
+    box, obox, st = _sys.fluid((L, L, L), 3.0, seed=3)
+    n = len(st[0])
+    e = _sys.engine(box, st)
+    e.setup()
+    e.step(10)
+    t = e.neighbor_table()
+    sel = np.random.default_rng(0).integers(0, n, 2000)
+    for i in sel:
+        c = t.core_row(i).astype(np.int64)
+        assert np.all(np.diff(c) > 0) and np.all(np.diff(t.skin_row(i).astype(np.int64)) > 0)
+        for j in c[:3]:
+            assert i in t.core_row(j) or i in t.skin_row(j)
+    mean_row = (t.core_count.astype(np.float64) + t.skin_count).mean()
+    assert 27.0 < mean_row < 28.3  # rho 4pi/3 1.3^3 = 27.6
+    F = np.stack(e.download().force, 1)
+    rms = np.sqrt((F ** 2).sum(1).mean())
+    assert np.abs(F.sum(0)).max() < 1e-5 * rms * np.sqrt(n)
+    assert abs(e.thermo()["kbt"] - 1.0) < 0.05
