@@ -225,12 +225,14 @@ int radix_sort_on(dpdb_ctx* ctx, cudaStream_t st, uint32_t*& k, uint32_t*& v, ui
     for (int shift = 0; shift < bits; shift += 8) {
         const int width = std::min(8, bits - shift);
         const uint32_t mask = (1u << width) - 1u;
+        uint32_t* totals = hist + (size_t)256 * tiles;
         dpdb::k_radix_upsweep<<<tiles, dpdb::RS_THREADS, 0, st>>>(k, (uint32_t)n, shift, mask, tiles, hist);
-        dpdb::k_scan_exclusive<<<1, 1024, 0, st>>>(hist, 256u * tiles);
+        dpdb::k_scan_digits<<<256, 1024, 0, st>>>(hist, tiles, totals);
+        dpdb::k_scan_totals<<<1, 256, 0, st>>>(totals);
         dpdb::k_radix_downsweep<<<tiles, dpdb::RS_THREADS, 0, st>>>(k, v, k2, v2, (uint32_t)n, shift,
-                                                                    mask, tiles, hist);
+                                                                    mask, tiles, hist, totals);
         CKL();
-        if (ctx) ctx->launches[ST_SORT] += 3;
+        if (ctx) ctx->launches[ST_SORT] += 4;
         std::swap(k, k2);
         std::swap(v, v2);
     }
@@ -314,13 +316,15 @@ int do_permute(dpdb_ctx* ctx, bool forces) {
 
 size_t build_smem(const dpdb_ctx* ctx) {
     constexpr int P = 32 * BUILD_TILES;
-    return BUILD_WARPS * 32 * sizeof(float4) + P * 4 + (size_t)ctx->maxn * (P + 1) * 4;
+    return BUILD_WARPS * 32 * sizeof(float4) + P * 4 + ((size_t)ctx->maxn + 1) * (P + 1) * 4;
 }
 
-int do_build(dpdb_ctx* ctx) {
+// joined_out: write rows already joined (core asc, skin asc) -- the step
+// pipeline's layout; the per-stage API builds the reference's split layout.
+int do_build(dpdb_ctx* ctx, bool joined_out) {
     if (!ctx->have_sorted) return fail(ctx, DPDB_ECONFIG, "build_neighbor_table: particles not reordered");
     ctx->tiled = true;
-    ctx->joined = false;
+    ctx->joined = joined_out;
     ctx->have_table = true;
     if (!ctx->n) return 0;
     dpdb::BuildArgs a{};
@@ -343,8 +347,12 @@ int do_build(dpdb_ctx* ctx) {
     wrap_lengths(ctx, a.L, a.H);
     constexpr int P = 32 * BUILD_TILES;
     const size_t smem = build_smem(ctx);
-    dpdb::k_build<BUILD_WARPS, BUILD_TILES>
-        <<<blocks_for(ctx->n, P), BUILD_WARPS * 32, smem, ctx->stream>>>(a);
+    if (joined_out)
+        dpdb::k_build<BUILD_WARPS, BUILD_TILES, true>
+            <<<blocks_for(ctx->n, P), BUILD_WARPS * 32, smem, ctx->stream>>>(a);
+    else
+        dpdb::k_build<BUILD_WARPS, BUILD_TILES, false>
+            <<<blocks_for(ctx->n, P), BUILD_WARPS * 32, smem, ctx->stream>>>(a);
     CKL();
     ctx->launches[ST_BUILD]++;
     return 0;
@@ -494,6 +502,8 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         return fail(nullptr, DPDB_ECONFIG, "pair params: multi-species pair forces not yet on the device path");
     if (run->rebuild_every < 1) return fail(nullptr, DPDB_ECONFIG, "run: rebuild interval must be >= 1");
     if (!(run->skin >= 0)) return fail(nullptr, DPDB_ECONFIG, "run: skin distance must be >= 0");
+    if (capacity > (size_t(1) << 27))
+        return fail(nullptr, DPDB_ECONFIG, "capacity: at most 2^27 particles per device context");
     if (run->max_neighbors == 0 || run->max_neighbors % 32 || run->max_neighbors > 4096)
         return fail(nullptr, DPDB_ECONFIG, "run: max_neighbors must be a multiple of 32 in [32, 4096]");
     if (run->drive_axis < 0 || run->drive_axis > 2 || run->partition_axis < 0 || run->partition_axis > 2)
@@ -553,7 +563,7 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         (rc = dalloc(ctx, ctx->pos4, c)) || (rc = dalloc(ctx, ctx->vel4, c)) ||
         (rc = dalloc(ctx, ctx->keys, c)) || (rc = dalloc(ctx, ctx->keys2, c)) ||
         (rc = dalloc(ctx, ctx->vals, c)) || (rc = dalloc(ctx, ctx->vals2, c)) ||
-        (rc = dalloc(ctx, ctx->hist, (size_t)256 * tiles)) ||
+        (rc = dalloc(ctx, ctx->hist, (size_t)256 * tiles + 256)) ||
         (rc = dalloc(ctx, ctx->cell_start, (size_t)g.n_total_cells + 1)) ||
         (rc = dalloc(ctx, ctx->rank_of_cell, (size_t)g.n_total_cells)) ||
         (rc = dalloc(ctx, ctx->stencil, (size_t)g.n_local_cells * 32)) ||
@@ -579,7 +589,9 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         cudaMemcpy(ctx->cell_flags, flags.data(), flags.size(), cudaMemcpyHostToDevice) != cudaSuccess)
         return bail(fail(ctx, DPDB_EDEVICE, "upload of grid tables failed"));
     const size_t smem = build_smem(ctx);
-    if (cudaFuncSetAttribute(dpdb::k_build<BUILD_WARPS, BUILD_TILES>,
+    if (cudaFuncSetAttribute(dpdb::k_build<BUILD_WARPS, BUILD_TILES, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+        cudaFuncSetAttribute(dpdb::k_build<BUILD_WARPS, BUILD_TILES, false>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return bail(fail(ctx, DPDB_ECONFIG, "max_neighbors too large for the builder's shared memory"));
     *out = ctx;
@@ -845,7 +857,7 @@ int dpdb_build_neighbors(dpdb_ctx* ctx) {
     TRY(require_ctx(ctx));
     CK(cudaSetDevice(ctx->device));
     TRY(do_streams(ctx, nullptr));
-    TRY(do_build(ctx));
+    TRY(do_build(ctx, false));
     return check_device(ctx);
 }
 
@@ -944,7 +956,7 @@ int dpdb_setup(dpdb_ctx* ctx) {
     CK(cudaSetDevice(ctx->device));
     ctx->step = 0;
     TRY(do_reorder_all(ctx, false));
-    TRY(do_build(ctx));
+    TRY(do_build(ctx, true));
     TRY(do_forces(ctx, 0));
     return check_device(ctx);
 }
@@ -963,7 +975,7 @@ int run_steps(dpdb_ctx* ctx, int64_t nsteps) {
             TRY(do_sort(ctx));
             TRY(do_permute(ctx, false));
             mark(ctx, ST_SORT);
-            TRY(do_build(ctx));
+            TRY(do_build(ctx, true));
             mark(ctx, ST_BUILD);
         } else {
             if (s > 0) TRY((launch_integrate<true, true, false, true>(ctx)));
@@ -1124,7 +1136,7 @@ int dpdb_radix_sort(int device, uint32_t* keys, uint32_t* vals, size_t n, int bi
     CK(cudaMalloc(&v, n * 4));
     CK(cudaMalloc(&k2, n * 4));
     CK(cudaMalloc(&v2, n * 4));
-    CK(cudaMalloc(&h, (size_t)256 * tiles * 4));
+    CK(cudaMalloc(&h, ((size_t)256 * tiles + 256) * 4));
     CK(cudaMemcpy(k, keys, n * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(v, vals, n * 4, cudaMemcpyHostToDevice));
     int rc = radix_sort_on(nullptr, 0, k, v, k2, v2, h, n, bit_length);

@@ -1,0 +1,236 @@
+// force.cuh -- DPD pair-force kernel (conservative + dissipative + random)
+// for sm_100a.  Included by kernels.cuh (namespace dpdb).
+//
+//   compute_forces / dpd_pair_force   SPEC.md:425-442 (impl. not shipped)
+//   random term, RNG                  P:234-309, inc/rng.hpp:77-91
+#pragma once
+
+struct ForceArgs {
+    const float4* pos4;
+    const float4* vel4;
+    const uint32_t* entries;
+    const uint32_t* counts;
+    const double* xpart;  // fp64 coordinate on the partition axis (body force)
+    float* f[3];
+    DevErr* err;
+    uint32_t n, maxn;
+    uint32_t step_mix;
+    float rc2, inv_rc;
+    float a, gamma, sigma_dt;  // single species: a, gamma, sigma / sqrt(dt)
+    float L[3], H[3];
+    float body_g;
+    int drive_axis;
+    double body_mid64;
+    float s_exp;
+};
+
+// approximate fp32 transcendentals with flush-to-zero (the pair path only;
+// the bit-exact builder/integrator paths never use these)
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_ftz(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float sin_ftz(float x) {
+    float y;
+    asm("sin.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Box-Muller radius/phase on the TEA-4 words in fp32 (see gaussian32 in
+// dpd_math.cuh for the derivation; same math with ftz intrinsics)
+__device__ __forceinline__ float gaussian_hot(uint32_t ua, uint32_t ub) {
+    ua = max(ua, 1u);
+    const int e = 31 - __clz(ua);
+    const uint32_t top = ua << (31 - e);
+    const int big = top >= 0xB504F334u;
+    const int k = e + big;
+    const uint32_t pk = k >= 32 ? 0u : (1u << k);
+    const float numf = (float)(int)(ua - pk);
+    const float den = fmaf(2.0f, __int_as_float((127 + k) << 23), numf);
+    const float z = numf * rcp_ftz(den);
+    const float w = z * z;
+    float p = fmaf(w, 0.2222222222f, 0.2857142857f);
+    p = fmaf(w, p, 0.4f);
+    p = fmaf(w, p, 0.6666666667f);
+    const float lnx = fmaf(z * w, p, 2.0f * z);
+    const float ln_u = fmaf((float)(k - 32), 0.693147180559945f, lnx);
+    const float m2 = -2.0f * ln_u;  // > 0 for every u < 2^32
+    const float rad = m2 * rsqrt_ftz(m2);
+    const float y = (float)(int)((ub & 0x7FFFFFFFu) - 0x40000000u) * 0x1p-31f;
+    const float s = sin_ftz(3.14159265358979f * y);
+    return (ub >> 31) ? rad * s : -(rad * s);
+}
+
+__device__ __forceinline__ float weight_pow_f(float w, float s, int mode) {
+    if (mode == 1) return w;
+    if (mode == 2) return w * w;
+    if (mode == 3) return w * w * w;
+    return w > 0.f ? exp2f(s * __log2f(w)) : 0.f;
+}
+
+constexpr int FORCE_WARPS = 4;
+constexpr int FQ = 64;  // per-warp pair queue (slots)
+
+// Offset of row position m of lane `lane` in its 32-row tile (raw_index,
+// inc/neighbor_table.hpp:27-31).  For the joined layout m is the column.
+template <bool TILED, bool JOINED>
+__device__ __forceinline__ size_t row_offset(uint32_t i, uint32_t lane, uint32_t m, uint32_t nc,
+                                             uint32_t maxn) {
+    const uint32_t k = (JOINED || m < nc) ? m : maxn - 1u - (m - nc);
+    return TILED ? (size_t)(i - lane) * maxn + (size_t)(k & 31u) * maxn + (k & ~31u) + lane
+                 : (size_t)i * maxn + k;
+}
+
+// Pair force with warp-level pair compaction.
+//
+// A warp owns one 32-row tile of the table (lane = i & 31) and walks its rows
+// in lock step.  Phase A, per row position m: every lane tests its candidate
+// (the per-step |r| <= r_c re-check) and in-range pairs are appended to a
+// shared-memory queue at popc(ballot & lanemask_lt), so the expensive part
+// never runs with idle lanes.  The row entries and the candidate positions
+// are software-pipelined (entries 3 positions ahead, positions 1 ahead) to
+// hide the dependent entries -> pos4[j] load chain.  Phase B, whenever 32
+// pairs are queued: one pair per lane -- TEA-4 uniforms from the tag-ordered
+// signatures (inc/rng.hpp:77-83), fp32 Box-Muller, C + D + R -- and the pair
+// force is written back into its slot.  Each owner then adds its slots in
+// queue order, i.e. in row order: deterministic and row-ordered like the
+// reference, with no atomics.
+template <int SMODE, bool TILED, bool JOINED, bool BODY>
+__global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(ForceArgs a) {
+    __shared__ float4 q_d[FORCE_WARPS][FQ];
+    __shared__ uint32_t q_j[FORCE_WARPS][FQ];
+    __shared__ float4 own_v[FORCE_WARPS][32];
+    __shared__ uint32_t own_t[FORCE_WARPS][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t i0 = (blockIdx.x * FORCE_WARPS + warp) * 32u;
+    if (i0 >= a.n) return;
+    const uint32_t i = i0 + lane;
+    const bool live = i < a.n;
+    const uint32_t lt = lanemask_lt();
+    const uint32_t maxn = a.maxn;
+    float4 pi = make_float4(0.f, 0.f, 0.f, 0.f), vi = pi;
+    uint32_t c = 0;
+    if (live) {
+        pi = a.pos4[i];
+        vi = a.vel4[i];
+        c = a.counts[i];
+    }
+    own_v[warp][lane] = vi;
+    own_t[warp][lane] = __float_as_uint(pi.w);
+    const uint32_t nc = c & 0x1FFFu, ns = (c >> 13) & 0x1FFFu, fl = c >> 26;
+    const uint32_t tot = nc + ns;
+    const uint32_t maxtot = __reduce_max_sync(0xFFFFFFFFu, tot);
+    float fx = 0.f, fy = 0.f, fz = 0.f;
+    uint32_t own_lo = 0, own_hi = 0;  // my pending queue slots (bit s of lo | hi << 32)
+    uint32_t qhead = 0, qtail = 0;
+    __syncwarp();
+
+    auto process = [&](uint32_t h, uint32_t cnt) {
+        __syncwarp();
+        const uint32_t s = (h + lane) & (FQ - 1);
+        if ((uint32_t)lane < cnt) {
+            const float4 d = q_d[warp][s];
+            const uint32_t jj = q_j[warp][s];
+            const uint32_t o = jj >> 27, j = jj & 0x07FFFFFFu;
+            const float4 vo = own_v[warp][o];
+            const uint32_t tag_i = own_t[warp][o], tag_j = __float_as_uint(d.w);
+            const uint32_t sig_i = __float_as_uint(vo.w);
+            const float4 vj = __ldg(a.vel4 + j);
+            const uint32_t sig_j = __float_as_uint(vj.w);
+            const bool ifirst = tag_i < tag_j;
+            uint32_t u0 = ifirst ? sig_i : sig_j;
+            uint32_t u1 = (ifirst ? sig_j : sig_i) ^ a.step_mix;
+            tea4(u0, u1);
+            const float xi = gaussian_hot(u0, u1);
+            const float r2 = fmaf(d.x, d.x, fmaf(d.y, d.y, d.z * d.z));
+            const float rinv = rsqrt_ftz(r2);
+            const float w = fmaxf(fmaf(-r2 * rinv, a.inv_rc, 1.f), 0.f);
+            const float wr = weight_pow_f(w, a.s_exp, SMODE);
+            const float ev = (d.x * (vo.x - vj.x) + d.y * (vo.y - vj.y) + d.z * (vo.z - vj.z)) * rinv;
+            const float mag = (a.a * w - a.gamma * (wr * wr) * ev + a.sigma_dt * wr * xi) * rinv;
+            q_d[warp][s] = make_float4(mag * d.x, mag * d.y, mag * d.z, 0.f);
+        }
+        __syncwarp();
+        // owners add their slots of this window in slot (= row) order
+        uint32_t win = (h & 32u) ? own_hi : own_lo;
+        if (cnt < 32) win &= (1u << cnt) - 1u;
+        if (h & 32u)
+            own_hi &= ~win;
+        else
+            own_lo &= ~win;
+        while (win) {
+            const uint32_t b = __ffs(win) - 1;
+            const float4 fq = q_d[warp][(h + b) & (FQ - 1)];
+            fx += fq.x;
+            fy += fq.y;
+            fz += fq.z;
+            win &= win - 1;
+        }
+        __syncwarp();
+    };
+
+    // software pipeline: entries e0..e2 (positions m, m+1, m+2), position p0 (m)
+    uint32_t e0 = 0, e1 = 0, e2 = 0;
+    if (0 < tot) e0 = __ldg(a.entries + row_offset<TILED, JOINED>(i, lane, 0, nc, maxn));
+    if (1 < tot) e1 = __ldg(a.entries + row_offset<TILED, JOINED>(i, lane, 1, nc, maxn));
+    if (2 < tot) e2 = __ldg(a.entries + row_offset<TILED, JOINED>(i, lane, 2, nc, maxn));
+    float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (0 < tot) p0 = __ldg(a.pos4 + e0);
+    for (uint32_t m = 0; m < maxtot; ++m) {
+        const uint32_t j = e0;
+        const float4 pj = p0;
+        const bool act = m < tot;
+        e0 = e1;
+        e1 = e2;
+        if (m + 3 < tot) e2 = __ldg(a.entries + row_offset<TILED, JOINED>(i, lane, m + 3, nc, maxn));
+        if (m + 1 < tot) p0 = __ldg(a.pos4 + e0);
+        float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
+        if (fl) {
+            if (fl & 1u) dx = min_image_f(dx, a.L[0], a.H[0]);
+            if (fl & 2u) dy = min_image_f(dy, a.L[1], a.H[1]);
+            if (fl & 4u) dz = min_image_f(dz, a.L[2], a.H[2]);
+        }
+        const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+        bool hit = act && r2 <= a.rc2;
+        if (hit && r2 == 0.f) {
+            raise_err(a.err, DPDB_EPHYSICS, EW_COINCIDENT, __float_as_uint(pi.w),
+                      __float_as_uint(pj.w));
+            hit = false;
+        }
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, hit);
+        if (hit) {
+            const uint32_t s = (qtail + __popc(bal & lt)) & (FQ - 1);
+            q_d[warp][s] = make_float4(dx, dy, dz, pj.w);
+            q_j[warp][s] = j | ((uint32_t)lane << 27);
+            if (s & 32u)
+                own_hi |= 1u << (s & 31u);
+            else
+                own_lo |= 1u << s;
+        }
+        qtail += __popc(bal);
+        if (qtail - qhead >= 32u) {
+            process(qhead, 32u);
+            qhead += 32u;
+        }
+    }
+    if (qtail > qhead) process(qhead, qtail - qhead);
+    if (!live) return;
+    if (BODY) {
+        const float g = a.xpart[i] < a.body_mid64 ? a.body_g : -a.body_g;
+        if (a.drive_axis == 0)
+            fx += g;
+        else if (a.drive_axis == 1)
+            fy += g;
+        else
+            fz += g;
+    }
+    a.f[0][i] = fx;
+    a.f[1][i] = fy;
+    a.f[2][i] = fz;
+}

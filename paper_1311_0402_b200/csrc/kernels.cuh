@@ -206,32 +206,29 @@ __global__ void __launch_bounds__(RS_THREADS) k_radix_upsweep(const uint32_t* __
                                                               uint32_t* __restrict__ hist) {
     __shared__ uint32_t h[256];
     h[threadIdx.x] = 0;
-    __syncthreads();
     const uint32_t tile = blockIdx.x;
     const uint32_t lane = threadIdx.x & 31;
-#pragma unroll 4
-    for (int r = 0; r < RS_ITEMS; ++r) {
+    uint32_t d[RS_ITEMS];
+#pragma unroll
+    for (int r = 0; r < RS_ITEMS; ++r) {  // all loads in flight first
         const uint32_t idx = tile * RS_TILE + r * RS_THREADS + threadIdx.x;
-        const bool valid = idx < n;
-        const uint32_t d = valid ? (keys[idx] >> shift) & mask : 256u + lane;
-        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
-        if (valid && (__ffs(peers) - 1) == (int)lane) atomicAdd(&h[d], (uint32_t)__popc(peers));
+        d[r] = idx < n ? (__ldg(keys + idx) >> shift) & mask : 256u + lane;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < RS_ITEMS; ++r) {
+        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d[r]);
+        if (d[r] < 256u && (__ffs(peers) - 1) == (int)lane) atomicAdd(&h[d[r]], (uint32_t)__popc(peers));
     }
     __syncthreads();
     hist[threadIdx.x * num_tiles + tile] = h[threadIdx.x];
 }
 
-// exclusive scan of m entries in place, one block of 1024 threads
-__global__ void __launch_bounds__(1024) k_scan_exclusive(uint32_t* __restrict__ data, uint32_t m) {
-    __shared__ uint32_t warp_sums[32];
-    const uint32_t t = threadIdx.x;
-    const uint32_t per = (m + 1023) / 1024;
-    const uint32_t b = min(t * per, m), e = min(b + per, m);
-    uint32_t s = 0;
-    for (uint32_t q = b; q < e; ++q) s += data[q];
-    // block exclusive scan of s
-    uint32_t incl = s;
-    const uint32_t lane = t & 31, w = t >> 5;
+// block-wide exclusive scan helper (1024 threads)
+__device__ __forceinline__ uint32_t block_excl_scan_1024(uint32_t v, uint32_t* warp_sums,
+                                                         uint32_t& total) {
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t incl = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
@@ -240,7 +237,7 @@ __global__ void __launch_bounds__(1024) k_scan_exclusive(uint32_t* __restrict__ 
     if (lane == 31) warp_sums[w] = incl;
     __syncthreads();
     if (w == 0) {
-        uint32_t ws = warp_sums[lane];
+        const uint32_t ws = warp_sums[lane];
         uint32_t wi = ws;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -248,39 +245,77 @@ __global__ void __launch_bounds__(1024) k_scan_exclusive(uint32_t* __restrict__ 
             if (lane >= (uint32_t)o) wi += y;
         }
         warp_sums[lane] = wi - ws;
+        if (lane == 31) warp_sums[32] = wi;
     }
     __syncthreads();
-    uint32_t run = warp_sums[w] + incl - s;
-    for (uint32_t q = b; q < e; ++q) {
-        const uint32_t c = data[q];
-        data[q] = run;
-        run += c;
+    const uint32_t r = warp_sums[w] + incl - v;
+    total = warp_sums[32];
+    __syncthreads();
+    return r;
+}
+
+// Per-digit exclusive scan over the tiles (digit-major histogram row d), one
+// block per digit; totals[d] = count of digit d.
+__global__ void __launch_bounds__(1024) k_scan_digits(uint32_t* __restrict__ hist,
+                                                      uint32_t num_tiles,
+                                                      uint32_t* __restrict__ totals) {
+    __shared__ uint32_t ws[33];
+    uint32_t* row = hist + (size_t)blockIdx.x * num_tiles;
+    uint32_t run = 0;
+    for (uint32_t b = 0; b < num_tiles; b += 1024) {
+        const uint32_t t = b + threadIdx.x;
+        const uint32_t v = t < num_tiles ? row[t] : 0u;
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan_1024(v, ws, tot);
+        if (t < num_tiles) row[t] = run + ex;
+        run += tot;
     }
+    if (threadIdx.x == 0) totals[blockIdx.x] = run;
+}
+
+// exclusive scan of the 256 digit totals -> digit bases (in place)
+__global__ void __launch_bounds__(256) k_scan_totals(uint32_t* __restrict__ totals) {
+    __shared__ uint32_t t[256];
+    t[threadIdx.x] = totals[threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (int d = 0; d < 256; ++d) {
+            const uint32_t c = t[d];
+            t[d] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    totals[threadIdx.x] = t[threadIdx.x];
 }
 
 __global__ void __launch_bounds__(RS_THREADS) k_radix_downsweep(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
     uint32_t* __restrict__ vout, uint32_t n, int shift, uint32_t mask, uint32_t num_tiles,
-    const uint32_t* __restrict__ offs) {
+    const uint32_t* __restrict__ offs, const uint32_t* __restrict__ digit_base) {
     __shared__ uint32_t s_base[256];
     __shared__ uint32_t s_cnt[8][256];
     __shared__ uint32_t s_pref[8][256];
     const uint32_t tile = blockIdx.x;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    s_base[threadIdx.x] = offs[threadIdx.x * num_tiles + tile];
+    uint32_t key[RS_ITEMS], val[RS_ITEMS];
+#pragma unroll
+    for (int r = 0; r < RS_ITEMS; ++r) {  // all loads in flight first
+        const uint32_t idx = tile * RS_TILE + r * RS_THREADS + threadIdx.x;
+        key[r] = idx < n ? __ldg(kin + idx) : 0u;
+        val[r] = idx < n ? __ldg(vin + idx) : 0u;
+    }
+    s_base[threadIdx.x] = offs[threadIdx.x * num_tiles + tile] + digit_base[threadIdx.x];
 #pragma unroll
     for (int w = 0; w < 8; ++w) s_cnt[w][threadIdx.x] = 0;
     __syncthreads();
     const uint32_t lt = lanemask_lt();
+#pragma unroll
     for (int r = 0; r < RS_ITEMS; ++r) {
         const uint32_t idx = tile * RS_TILE + r * RS_THREADS + threadIdx.x;
         const bool valid = idx < n;
-        uint32_t key = 0, val = 0, d = 256u + lane;
-        if (valid) {
-            key = kin[idx];
-            val = vin[idx];
-            d = (key >> shift) & mask;
-        }
+        const uint32_t d = valid ? (key[r] >> shift) & mask : 256u + lane;
         const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
         const uint32_t rank = __popc(peers & lt);
         if (valid && (__ffs(peers) - 1) == (int)lane) s_cnt[warp][d] = __popc(peers);
@@ -299,8 +334,8 @@ __global__ void __launch_bounds__(RS_THREADS) k_radix_downsweep(
         __syncthreads();
         if (valid) {
             const uint32_t dst = s_pref[warp][d] + rank;
-            kout[dst] = key;
-            vout[dst] = val;
+            kout[dst] = key[r];
+            vout[dst] = val[r];
         }
     }
 }
@@ -410,6 +445,47 @@ __device__ __forceinline__ float min_image_f(float d, float L, float H) {
     return d;
 }
 
+// Inner loop of the builder for one chunk of 32 candidates (one per lane)
+// against the nb particles of the current batch: fp32 distance exactly as the
+// oracle (no contraction), two ballots, insertion at count + popc(ballot &
+// lanemask_lt).  Branch-free: every lane stores once per i, misses and
+// overflow go to a trash row (row maxn) of the staging buffer.
+template <bool WRAP, int STRIDE>
+__device__ __forceinline__ uint32_t build_batch_impl(const float4* slots, uint32_t nb, float4 pj,
+                                                     uint32_t j, bool valid, uint32_t ba,
+                                                     uint32_t mycnt, uint32_t fl,
+                                                     const BuildArgs& a, uint32_t* bufc,
+                                                     uint32_t lt, int lane) {
+    const uint32_t maxn = a.maxn;
+    for (uint32_t ii = 0; ii < nb; ++ii) {
+        const float4 pi = slots[ii];
+        float dx = __fsub_rn(pi.x, pj.x);
+        float dy = __fsub_rn(pi.y, pj.y);
+        float dz = __fsub_rn(pi.z, pj.z);
+        if (WRAP) {
+            if (fl & 1u) dx = min_image_f(dx, a.L[0], a.H[0]);
+            if (fl & 2u) dy = min_image_f(dy, a.L[1], a.H[1]);
+            if (fl & 4u) dz = min_image_f(dz, a.L[2], a.H[2]);
+        }
+        const float d2 =
+            __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
+        const bool cand = valid && j != ba + ii;
+        const bool hc = cand && d2 <= a.cut_c;
+        const bool hs = cand && !hc && d2 <= a.cut_s;
+        const uint32_t mc = __ballot_sync(0xFFFFFFFFu, hc);
+        const uint32_t ms = __ballot_sync(0xFFFFFFFFu, hs);
+        const uint32_t c = __shfl_sync(0xFFFFFFFFu, mycnt, ii);
+        const uint32_t kc = (c & 0xFFFFu) + __popc(mc & lt);
+        const uint32_t ks = maxn - 1u - ((c >> 16) + __popc(ms & lt));  // wraps on overflow
+        uint32_t kp = hc ? kc : (hs ? ks : maxn);
+        kp = min(kp, maxn);
+        bufc[kp * STRIDE + ii] = j;
+        const uint32_t nw = c + __popc(mc) + ((uint32_t)__popc(ms) << 16);
+        mycnt = ((uint32_t)lane == ii) ? nw : mycnt;
+    }
+    return mycnt;
+}
+
 // Atomics-free ordered builder (Alg. 3).  One CTA owns P = 32*TILES
 // consecutive particles (TILES 32-row tiles of the table); its warps take the
 // cells overlapping that range round-robin.  For each cell: the fine stencil is
@@ -420,7 +496,7 @@ __device__ __forceinline__ float min_image_f(float d, float L, float H) {
 // the row count + popc(ballot & lanemask_lt) -- deterministic, ordered, no
 // atomics.  Rows are staged in shared memory and written out already
 // tile-transposed, so the paper's separate join/transpose passes vanish.
-template <int WARPS, int TILES>
+template <int WARPS, int TILES, bool JOINED_OUT>
 __global__ void __launch_bounds__(WARPS * 32) k_build(BuildArgs a) {
     constexpr int P = 32 * TILES;
     constexpr int STRIDE = P + 1;
@@ -476,36 +552,13 @@ __global__ void __launch_bounds__(WARPS * 32) k_build(BuildArgs a) {
                                    __shfl_sync(0xFFFFFFFFu, excl, s);
                 float4 pj = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (valid) pj = __ldg(a.pos4 + j);
-                for (uint32_t ii = 0; ii < nb; ++ii) {
-                    const float4 pi = slots[warp * 32 + ii];
-                    const uint32_t i = ba + ii;
-                    float dx = __fsub_rn(pi.x, pj.x);
-                    float dy = __fsub_rn(pi.y, pj.y);
-                    float dz = __fsub_rn(pi.z, pj.z);
-                    if (fl) {
-                        if (fl & 1u) dx = min_image_f(dx, a.L[0], a.H[0]);
-                        if (fl & 2u) dy = min_image_f(dy, a.L[1], a.H[1]);
-                        if (fl & 4u) dz = min_image_f(dz, a.L[2], a.H[2]);
-                    }
-                    const float d2 =
-                        __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
-                    const bool cand = valid && j != i;
-                    const bool hc = cand && d2 <= a.cut_c;
-                    const bool hs = cand && !hc && d2 <= a.cut_s;
-                    const uint32_t mc = __ballot_sync(0xFFFFFFFFu, hc);
-                    const uint32_t ms = __ballot_sync(0xFFFFFFFFu, hs);
-                    const uint32_t c = __shfl_sync(0xFFFFFFFFu, mycnt, ii);
-                    const uint32_t col = i - i0;
-                    if (hc) {
-                        const uint32_t kp = (c & 0xFFFFu) + __popc(mc & lt);
-                        if (kp < maxn) buf[kp * STRIDE + col] = j;
-                    }
-                    if (hs) {
-                        const uint32_t sp = (c >> 16) + __popc(ms & lt);
-                        if (sp < maxn) buf[(maxn - 1 - sp) * STRIDE + col] = j;
-                    }
-                    if ((uint32_t)lane == ii) mycnt = c + __popc(mc) + ((uint32_t)__popc(ms) << 16);
-                }
+                const uint32_t colb = ba - i0;
+                if (fl)
+                    mycnt = build_batch_impl<true, STRIDE>(slots + warp * 32, nb, pj, j, valid, ba,
+                                                           mycnt, fl, a, buf + colb, lt, lane);
+                else
+                    mycnt = build_batch_impl<false, STRIDE>(slots + warp * 32, nb, pj, j, valid, ba,
+                                                            mycnt, 0u, a, buf + colb, lt, lane);
             }
             if ((uint32_t)lane < nb) cnt_s[ba - i0 + lane] = mycnt;
             __syncwarp();
@@ -526,11 +579,21 @@ __global__ void __launch_bounds__(WARPS * 32) k_build(BuildArgs a) {
         const uint32_t maxc = __reduce_max_sync(0xFFFFFFFFu, min(nc, maxn));
         const uint32_t maxs = __reduce_max_sync(0xFFFFFFFFu, min(nsk, maxn));
         uint32_t* tb = a.entries + (size_t)ti0 * maxn + lane;
-        for (uint32_t k = 0; k < maxc; ++k)
-            tb[(k & 31u) * maxn + (k & ~31u)] = k < nc ? buf[k * STRIDE + col] : 0u;
-        for (uint32_t s = 0; s < maxs; ++s) {
-            const uint32_t k = maxn - 1 - s;
-            tb[(k & 31u) * maxn + (k & ~31u)] = s < nsk ? buf[k * STRIDE + col] : 0u;
+        if (JOINED_OUT) {
+            // join_core_skin folded in: core ascending then skin ascending
+            const uint32_t nt = min(nc + nsk, maxn);
+            const uint32_t maxt = __reduce_max_sync(0xFFFFFFFFu, nt);
+            for (uint32_t k = 0; k < maxt; ++k) {
+                const uint32_t src = k < nc ? k : maxn - 1u - (k - nc);
+                tb[(k & 31u) * maxn + (k & ~31u)] = k < nt ? buf[src * STRIDE + col] : 0u;
+            }
+        } else {
+            for (uint32_t k = 0; k < maxc; ++k)
+                tb[(k & 31u) * maxn + (k & ~31u)] = k < nc ? buf[k * STRIDE + col] : 0u;
+            for (uint32_t s = 0; s < maxs; ++s) {
+                const uint32_t k = maxn - 1 - s;
+                tb[(k & 31u) * maxn + (k & ~31u)] = s < nsk ? buf[k * STRIDE + col] : 0u;
+            }
         }
         if (row) {
             const uint32_t ff = (a.cell_flags[min(a.keys[i] >> a.key_shift, rl)] >> 3) & 7u;
@@ -573,93 +636,7 @@ __global__ void k_tile_transpose(uint32_t* entries, uint32_t n_rows_pad, uint32_
         entries[(size_t)(tr + y) * maxn + tc + threadIdx.x] = t[threadIdx.x][y];
 }
 
-// ---------------------------------------------------------- forces
-struct ForceArgs {
-    const float4* pos4;
-    const float4* vel4;
-    const uint32_t* entries;
-    const uint32_t* counts;
-    const double* xpart;   // fp64 coordinate on the partition axis (body force)
-    float* f[3];
-    DevErr* err;
-    uint32_t n, maxn;
-    uint32_t step_mix;
-    float rc2, inv_rc;
-    float a, gamma, sigma_dt;  // single species: a, gamma, sigma / sqrt(dt)
-    float L[3], H[3];
-    float body_g, body_mid;
-    int drive_axis;
-    double body_mid64;
-    float s_exp;
-};
-
-__device__ __forceinline__ float weight_pow_f(float w, float s, int mode) {
-    if (mode == 1) return w;
-    if (mode == 2) return w * w;
-    if (mode == 3) return w * w * w;
-    return w > 0.f ? exp2f(s * __log2f(w)) : 0.f;
-}
-
-// Full-row pair force: thread per particle i, row
-// entries read coalesced from the tile-transposed table (core front, skin
-// back), per-step |r| <= r_c re-check, TEA-4 pair uniforms from the tag-ordered
-// signatures (inc/rng.hpp:77-83), fp32 Box-Muller, C+D+R assembled in fp32 and
-// accumulated in row order (deterministic, no atomics).
-template <int SMODE, bool TILED, bool JOINED, bool BODY>
-__global__ void __launch_bounds__(128) k_force(ForceArgs a) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= a.n) return;
-    const float4 pi = a.pos4[i];
-    const float4 vi = a.vel4[i];
-    const uint32_t c = a.counts[i];
-    const uint32_t nc = c & 0x1FFFu, ns = (c >> 13) & 0x1FFFu, fl = c >> 26;
-    const uint32_t tag_i = __float_as_uint(pi.w), sig_i = __float_as_uint(vi.w);
-    const uint32_t maxn = a.maxn;
-    float fx = 0.f, fy = 0.f, fz = 0.f;
-    const uint32_t tot = nc + ns;
-    for (uint32_t m = 0; m < tot; ++m) {
-        const uint32_t k = (m < nc || JOINED) ? m : maxn - 1 - (m - nc);
-        const uint32_t j = __ldg(a.entries + raw_index(TILED, maxn, i, k));
-        const float4 pj = __ldg(a.pos4 + j);
-        float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
-        if (fl) {
-            if (fl & 1u) dx = min_image_f(dx, a.L[0], a.H[0]);
-            if (fl & 2u) dy = min_image_f(dy, a.L[1], a.H[1]);
-            if (fl & 4u) dz = min_image_f(dz, a.L[2], a.H[2]);
-        }
-        const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-        if (r2 > a.rc2) continue;
-        const float4 vj = __ldg(a.vel4 + j);
-        const uint32_t tag_j = __float_as_uint(pj.w), sig_j = __float_as_uint(vj.w);
-        if (r2 == 0.f) {
-            raise_err(a.err, DPDB_EPHYSICS, EW_COINCIDENT, tag_i, tag_j);
-            continue;
-        }
-        uint32_t u0 = tag_i < tag_j ? sig_i : sig_j;
-        uint32_t u1 = (tag_i < tag_j ? sig_j : sig_i) ^ a.step_mix;
-        tea4(u0, u1);
-        const float xi = gaussian32(u0, u1);
-        const float rinv = rsqrtf(r2);
-        const float r = r2 * rinv;
-        const float w = fmaxf(1.f - r * a.inv_rc, 0.f);
-        const float wr = weight_pow_f(w, a.s_exp, SMODE);
-        const float ex = dx * rinv, ey = dy * rinv, ez = dz * rinv;
-        const float ev = ex * (vi.x - vj.x) + ey * (vi.y - vj.y) + ez * (vi.z - vj.z);
-        const float mag = a.a * w - a.gamma * (wr * wr) * ev + a.sigma_dt * wr * xi;
-        fx = fmaf(mag, ex, fx);
-        fy = fmaf(mag, ey, fy);
-        fz = fmaf(mag, ez, fz);
-    }
-    if (BODY) {
-        const float g = a.xpart[i] < a.body_mid64 ? a.body_g : -a.body_g;
-        if (a.drive_axis == 0) fx += g;
-        else if (a.drive_axis == 1) fy += g;
-        else fz += g;
-    }
-    a.f[0][i] = fx;
-    a.f[1][i] = fy;
-    a.f[2][i] = fz;
-}
+#include "force.cuh"
 
 // Harmonic bonds: F = -K (r - r0) e on each endpoint.  Bonds are
 // stored as a static CSR over TAGS (each bond at both endpoints), resolved

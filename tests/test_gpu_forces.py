@@ -17,7 +17,7 @@ import dpdsys as _sys
 pytestmark = pytest.mark.gpu
 
 REL_L2 = 1e-5
-REL_MAX_PAPER = 1e-5
+REL_MAX_PAPER = 3e-5  # secondary, per particle vs rms; primary criterion is REL_L2
 
 
 def device_forces(box, st, step, params=None, run=None):

@@ -11,7 +11,7 @@ pytestmark = pytest.mark.gpu
 
 
 def f32_forces(n, seed):
-    return [np.random.default_rng(seed + k).normal(size=n).astype(np.float32).astype(np.float64) * 20
+    return [(np.random.default_rng(seed + k).normal(size=n) * 20).astype(np.float32).astype(np.float64)
             for k in range(3)]
 
 
@@ -49,29 +49,71 @@ def test_blowup_is_physics_error():
     assert ex.value.code == 2
 
 
-def test_short_trajectory_vs_oracle():
-    """setup + 20 steps (two rebuilds) on the device vs the oracle's Alg. 1 driver."""
+def test_fused_step_equals_stagewise_api():
+    """dpdb_step's fused kernels (phase2+phase1+streams, reorder, build, force)
+    reproduce the stage-by-stage ABI sequence of Alg. 1 bit for bit."""
     box, obox, st = _sys.fluid((12, 12, 12), 3.0, seed=21)
-    p = dpd.PairParams()
+    a = _sys.engine(box, st)
+    a.setup()
+    b = _sys.engine(box, st)
+    b.reorder_particles()
+    b.build_neighbor_table()
+    b.compute_forces(0)
+    for step in range(1, 26):
+        a.step(1)
+        b.verlet_phase1()
+        if step % 10 == 0:
+            b.reorder_particles()
+            b.build_neighbor_table()
+        b.compute_forces(step)
+        b.verlet_phase2()
+    sa, sb = a.download(), b.download()
+    assert np.array_equal(sa.tag, sb.tag)
+    for u, w in zip(sa.coord + sa.veloc + sa.force, sb.coord + sb.veloc + sb.force):
+        assert np.array_equal(u, w)
+    c = _sys.engine(box, st)  # one call of 25 steps == 25 calls of one step
+    c.setup()
+    c.step(25)
+    sc = c.download()
+    for u, w in zip(sa.coord + sa.veloc, sc.coord + sc.veloc):
+        assert np.array_equal(u, w)
+
+
+def test_first_step_vs_oracle_driver():
+    """Setup + one step against the oracle's Alg. 1 driver.  After one step
+    the fp64 positions agree to fp32-force rounding; beyond that trajectories
+    are compared statistically only (a velocity differing in its 11 leading
+    mantissa bits changes a signature, P:241-266 / SURVEY hard part 4)."""
+    box, obox, st = _sys.fluid((12, 12, 12), 3.0, seed=21)
     e = _sys.engine(box, st)
     e.setup()
-    e.step(20)
-    assert e.current_step == 20
+    e.step(1)
     s = e.download()
-    sim = O.Sim(obox, _sys.oparams(p), st, nthreads=8)
-    sim.run(20)
+    sim = O.Sim(obox, _sys.oparams(dpd.PairParams()), st, nthreads=8)
+    sim.run(1)
     r = sim.state()
-    og = np.argsort(s.tag)
-    orr = np.argsort(r["tag"])
-    L = 12.0
+    og, orr = np.argsort(s.tag), np.argsort(r["tag"])
     for k, key in enumerate("xyz"):
         d = s.coord[k][og] - r[key][orr]
-        d -= L * np.round(d / L)
-        assert np.abs(d).max() < 1e-5, (key, np.abs(d).max())
-    for k, key in enumerate(["vx", "vy", "vz"]):
-        assert np.abs(s.veloc[k][og] - r[key][orr]).max() < 1e-3
-    th = e.thermo()
-    assert th["kbt"] == pytest.approx(sim.temperature(), rel=1e-4)
+        d -= 12.0 * np.round(d / 12.0)
+        assert np.abs(d).max() < 1e-7
+
+
+def test_long_run_statistics_vs_oracle():
+    box, obox, st = _sys.fluid((10, 10, 10), 3.0, seed=22)
+    e = _sys.engine(box, st)
+    e.setup()
+    sim = O.Sim(obox, _sys.oparams(dpd.PairParams()), st, nthreads=8)
+    e.step(300)
+    sim.run(300)
+    tg, to = [], []
+    for _ in range(20):
+        e.step(10)
+        sim.run(10)
+        tg.append(e.thermo()["kbt"])
+        to.append(sim.temperature())
+    assert abs(np.mean(tg) - 1.0) < 0.03 and abs(np.mean(to) - 1.0) < 0.03
+    assert abs(np.mean(tg) - np.mean(to)) < 0.03
 
 
 def test_thermostat_c1():
@@ -97,7 +139,7 @@ def test_c3_properties_4m():
     n = len(st[0])
     e = _sys.engine(box, st)
     e.setup()
-    e.step(10)
+    e.step(300)
     t = e.neighbor_table()
     sel = np.random.default_rng(0).integers(0, n, 2000)
     for i in sel:
@@ -106,7 +148,7 @@ def test_c3_properties_4m():
         for j in c[:3]:
             assert i in t.core_row(j) or i in t.skin_row(j)
     mean_row = (t.core_count.astype(np.float64) + t.skin_count).mean()
-    assert 27.0 < mean_row < 28.3  # rho 4pi/3 1.3^3 = 27.6
+    assert 25.0 < mean_row < 28.3  # ideal gas: rho 4pi/3 1.3^3 = 27.6; a=25 depletes g(r<1)
     F = np.stack(e.download().force, 1)
     rms = np.sqrt((F ** 2).sum(1).mean())
     assert np.abs(F.sum(0)).max() < 1e-5 * rms * np.sqrt(n)
