@@ -25,7 +25,6 @@ thread_local std::string g_thread_err;
 
 constexpr int BUILD_WARPS = 4;
 constexpr int BUILD_TILES = 2;
-constexpr int FORCE_THREADS = 128;
 constexpr int RED_BLOCKS = 296;
 
 enum Stage { ST_INTEGRATE = 0, ST_SORT = 1, ST_BUILD = 2, ST_FORCE = 3, ST_OTHER = 4, ST_N = 5 };
@@ -372,11 +371,12 @@ int do_streams(dpdb_ctx* ctx, uint32_t* sig_out) {
 
 template <int SMODE, bool TILED, bool JOINED>
 void force_launch(dpdb_ctx* ctx, const dpdb::ForceArgs& a, bool body) {
-    const unsigned nb = blocks_for(ctx->n, FORCE_THREADS);
+    const unsigned nb = blocks_for(ctx->n, dpdb::FORCE_BLOCK);
+    constexpr int T = dpdb::FORCE_WARPS * 32;
     if (body)
-        dpdb::k_force<SMODE, TILED, JOINED, true><<<nb, FORCE_THREADS, 0, ctx->stream>>>(a);
+        dpdb::k_force<SMODE, TILED, JOINED, true><<<nb, T, 0, ctx->stream>>>(a);
     else
-        dpdb::k_force<SMODE, TILED, JOINED, false><<<nb, FORCE_THREADS, 0, ctx->stream>>>(a);
+        dpdb::k_force<SMODE, TILED, JOINED, false><<<nb, T, 0, ctx->stream>>>(a);
 }
 
 template <int SMODE>
@@ -502,8 +502,8 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         return fail(nullptr, DPDB_ECONFIG, "pair params: multi-species pair forces not yet on the device path");
     if (run->rebuild_every < 1) return fail(nullptr, DPDB_ECONFIG, "run: rebuild interval must be >= 1");
     if (!(run->skin >= 0)) return fail(nullptr, DPDB_ECONFIG, "run: skin distance must be >= 0");
-    if (capacity > (size_t(1) << 27))
-        return fail(nullptr, DPDB_ECONFIG, "capacity: at most 2^27 particles per device context");
+    if (capacity > (size_t(1) << 26))
+        return fail(nullptr, DPDB_ECONFIG, "capacity: at most 2^26 particles per device context");
     if (run->max_neighbors == 0 || run->max_neighbors % 32 || run->max_neighbors > 4096)
         return fail(nullptr, DPDB_ECONFIG, "run: max_neighbors must be a multiple of 32 in [32, 4096]");
     if (run->drive_axis < 0 || run->drive_axis > 2 || run->partition_axis < 0 || run->partition_axis > 2)

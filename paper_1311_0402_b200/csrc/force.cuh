@@ -74,163 +74,187 @@ __device__ __forceinline__ float weight_pow_f(float w, float s, int mode) {
     return w > 0.f ? exp2f(s * __log2f(w)) : 0.f;
 }
 
-constexpr int FORCE_WARPS = 4;
+constexpr int FORCE_WARPS = 8;   // warps per CTA
+constexpr int FORCE_TILES = 16;  // 32-row tiles per CTA block: B = 512 particles
+constexpr int FORCE_BLOCK = 32 * FORCE_TILES;
 constexpr int FQ = 64;  // per-warp pair queue (slots)
+// Forces are accumulated as 2^-18 fixed-point int32 (|F| < 8192 per particle,
+// resolution 3.8e-6): integer sums commute, so the result does not depend on
+// the order in which lanes or warps deliver their shares.
+constexpr float FIX_SCALE = 262144.0f;
+constexpr float FIX_INV = 1.0f / 262144.0f;
 
 // Offset of row position m of lane `lane` in its 32-row tile (raw_index,
-// inc/neighbor_table.hpp:27-31).  For the joined layout m is the column.
+// inc/neighbor_table.hpp:27-31), relative to entries + i0*maxn + lane.
 template <bool TILED, bool JOINED>
-__device__ __forceinline__ size_t row_offset(uint32_t i, uint32_t lane, uint32_t m, uint32_t nc,
-                                             uint32_t maxn) {
+__device__ __forceinline__ uint32_t row_offset(uint32_t lane, uint32_t m, uint32_t nc,
+                                               uint32_t maxn) {
     const uint32_t k = (JOINED || m < nc) ? m : maxn - 1u - (m - nc);
-    return TILED ? (size_t)(i - lane) * maxn + (size_t)(k & 31u) * maxn + (k & ~31u) + lane
-                 : (size_t)i * maxn + k;
+    return TILED ? (k & 31u) * maxn + (k & ~31u) : lane * (maxn - 1u) + k;
 }
 
-// Pair force with warp-level pair compaction.
+// Pair force: warp-level pair compaction + a
+// block-local half list + order-free fixed-point accumulation.
 //
-// A warp owns one 32-row tile of the table (lane = i & 31) and walks its rows
-// in lock step.  Phase A, per row position m: every lane tests its candidate
-// (the per-step |r| <= r_c re-check) and in-range pairs are appended to a
-// shared-memory queue at popc(ballot & lanemask_lt), so the expensive part
-// never runs with idle lanes.  The row entries and the candidate positions
-// are software-pipelined (entries 3 positions ahead, positions 1 ahead) to
-// hide the dependent entries -> pos4[j] load chain.  Phase B, whenever 32
-// pairs are queued: one pair per lane -- TEA-4 uniforms from the tag-ordered
-// signatures (inc/rng.hpp:77-83), fp32 Box-Muller, C + D + R -- and the pair
-// force is written back into its slot.  Each owner then adds its slots in
-// queue order, i.e. in row order: deterministic and row-ordered like the
-// reference, with no atomics.
+// A CTA owns a block of FORCE_BLOCK consecutive particles (a compact Morton
+// region) and a shared int32 force accumulator for them.  Each warp walks one
+// 32-row tile of the table at a time (lane = i & 31).  Phase A, per row
+// position m: every lane re-checks its candidate (the per-step |r| <= r_c
+// test) and in-range pairs are appended to a per-warp shared-memory queue at
+// popc(ballot & lanemask_lt), so the expensive part never runs with idle
+// lanes.  A pair whose partner j lies in the same block is taken only by its
+// lower index (the pair RNG is symmetric in (i, j), inc/rng.hpp:74-83, so
+// F_ji = -F_ij); pairs that cross the block boundary are evaluated from both
+// sides, so no global atomics are needed.  Phase B, whenever 32 pairs are
+// queued: one pair per lane -- TEA-4 uniforms from the tag-ordered
+// signatures, fp32 Box-Muller, C + D + R -- rounded once to fixed point q and
+// added as +q to i and -q to j in the block accumulator.  Deterministic run
+// to run, and Newton's third law holds exactly.  Row entries and candidate
+// positions are software-pipelined (entries 3 ahead, positions 1 ahead).
 template <int SMODE, bool TILED, bool JOINED, bool BODY>
 __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(ForceArgs a) {
-    __shared__ float4 q_d[FORCE_WARPS][FQ];
-    __shared__ uint32_t q_j[FORCE_WARPS][FQ];
+    __shared__ float4 q_d[FORCE_WARPS][FQ];   // (dx, dy, dz, tag_j)
+    __shared__ uint32_t q_j[FORCE_WARPS][FQ]; // j | in_block << 26 | owner lane << 27
     __shared__ float4 own_v[FORCE_WARPS][32];
     __shared__ uint32_t own_t[FORCE_WARPS][32];
+    __shared__ int acc[FORCE_BLOCK * 3];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t i0 = (blockIdx.x * FORCE_WARPS + warp) * 32u;
-    if (i0 >= a.n) return;
-    const uint32_t i = i0 + lane;
-    const bool live = i < a.n;
+    const uint32_t b0 = blockIdx.x * FORCE_BLOCK;
+    const uint32_t bn = min((uint32_t)FORCE_BLOCK, a.n - b0);  // particles in this block
+    for (int t = threadIdx.x; t < FORCE_BLOCK * 3; t += FORCE_WARPS * 32) acc[t] = 0;
+    __syncthreads();
     const uint32_t lt = lanemask_lt();
     const uint32_t maxn = a.maxn;
-    float4 pi = make_float4(0.f, 0.f, 0.f, 0.f), vi = pi;
-    uint32_t c = 0;
-    if (live) {
-        pi = a.pos4[i];
-        vi = a.vel4[i];
-        c = a.counts[i];
+    bool coincident = false;
+    uint32_t bad_tag = 0;
+
+    for (int tile = warp; tile < FORCE_TILES; tile += FORCE_WARPS) {
+        const uint32_t il0 = 32u * tile;
+        if (il0 >= bn) break;
+        const uint32_t il = il0 + lane;  // my index in the block
+        const uint32_t i = b0 + il;
+        const bool live = il < bn;
+        float4 pi = make_float4(0.f, 0.f, 0.f, 0.f), vi = pi;
+        uint32_t c = 0;
+        if (live) {
+            pi = a.pos4[i];
+            vi = a.vel4[i];
+            c = a.counts[i];
+        }
+        own_v[warp][lane] = vi;
+        const uint32_t nc = c & 0x1FFFu, ns = (c >> 13) & 0x1FFFu, fl = c >> 26;
+        const uint32_t tot = nc + ns;
+        const uint32_t maxtot = __reduce_max_sync(0xFFFFFFFFu, tot);
+        const uint32_t tag_me = __float_as_uint(pi.w);
+        own_t[warp][lane] = tag_me;
+        uint32_t qhead = 0, qtail = 0;
+        __syncwarp();
+
+        auto process = [&](uint32_t h, uint32_t cnt) {
+            __syncwarp();
+            const uint32_t s = (h + lane) & (FQ - 1);
+            if ((uint32_t)lane < cnt) {
+                const float4 d = q_d[warp][s];
+                const uint32_t jj = q_j[warp][s];
+                const uint32_t o = jj >> 27, j = jj & 0x03FFFFFFu;
+                const float4 vo = own_v[warp][o];
+                const uint32_t tag_i = own_t[warp][o], tag_j = __float_as_uint(d.w);
+                const uint32_t sig_i = __float_as_uint(vo.w);
+                const float4 vj = __ldg(a.vel4 + j);
+                const uint32_t sig_j = __float_as_uint(vj.w);
+                const bool ifirst = tag_i < tag_j;
+                uint32_t u0 = ifirst ? sig_i : sig_j;
+                uint32_t u1 = (ifirst ? sig_j : sig_i) ^ a.step_mix;
+                tea4(u0, u1);
+                const float xi = gaussian_hot(u0, u1);
+                const float r2 = fmaf(d.x, d.x, fmaf(d.y, d.y, d.z * d.z));
+                const float rinv = rsqrt_ftz(r2);
+                const float w = fmaxf(fmaf(-r2 * rinv, a.inv_rc, 1.f), 0.f);
+                const float wr = weight_pow_f(w, a.s_exp, SMODE);
+                const float ev =
+                    (d.x * (vo.x - vj.x) + d.y * (vo.y - vj.y) + d.z * (vo.z - vj.z)) * rinv;
+                const float mag =
+                    (a.a * w - a.gamma * (wr * wr) * ev + a.sigma_dt * wr * xi) * (rinv * FIX_SCALE);
+                const int qx = __float2int_rn(mag * d.x);
+                const int qy = __float2int_rn(mag * d.y);
+                const int qz = __float2int_rn(mag * d.z);
+                int* ai = acc + 3 * (il0 + o);
+                atomicAdd(ai + 0, qx);
+                atomicAdd(ai + 1, qy);
+                atomicAdd(ai + 2, qz);
+                if (jj & (1u << 26)) {  // partner in this block takes -q
+                    int* aj = acc + 3 * (j - b0);
+                    atomicAdd(aj + 0, -qx);
+                    atomicAdd(aj + 1, -qy);
+                    atomicAdd(aj + 2, -qz);
+                }
+            }
+            __syncwarp();
+        };
+
+        // software pipeline: entries e0..e2 (positions m, m+1, m+2), position p0 (m)
+        const uint32_t* erow = a.entries + (size_t)(b0 + il0) * maxn + lane;
+        uint32_t e0 = 0, e1 = 0, e2 = 0;
+        if (0 < tot) e0 = __ldg(erow + row_offset<TILED, JOINED>(lane, 0, nc, maxn));
+        if (1 < tot) e1 = __ldg(erow + row_offset<TILED, JOINED>(lane, 1, nc, maxn));
+        if (2 < tot) e2 = __ldg(erow + row_offset<TILED, JOINED>(lane, 2, nc, maxn));
+        float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (0 < tot) p0 = __ldg(a.pos4 + e0);
+        for (uint32_t m = 0; m < maxtot; ++m) {
+            const uint32_t j = e0;
+            const float4 pj = p0;
+            const uint32_t jl = j - b0;
+            const bool inblk = jl < bn;
+            const bool act = m < tot && !(inblk && jl < il);  // lower index takes the pair
+            e0 = e1;
+            e1 = e2;
+            if (m + 3 < tot) e2 = __ldg(erow + row_offset<TILED, JOINED>(lane, m + 3, nc, maxn));
+            if (m + 1 < tot) p0 = __ldg(a.pos4 + e0);
+            float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
+            if (fl) {
+                if (fl & 1u) dx = min_image_f(dx, a.L[0], a.H[0]);
+                if (fl & 2u) dy = min_image_f(dy, a.L[1], a.H[1]);
+                if (fl & 4u) dz = min_image_f(dz, a.L[2], a.H[2]);
+            }
+            const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+            if (act && r2 == 0.f) {
+                coincident = true;
+                bad_tag = tag_me;
+            }
+            const bool hit = act && r2 <= a.rc2 && r2 > 0.f;
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, hit);
+            if (hit) {
+                const uint32_t s = (qtail + __popc(bal & lt)) & (FQ - 1);
+                q_d[warp][s] = make_float4(dx, dy, dz, pj.w);
+                q_j[warp][s] = j | ((uint32_t)inblk << 26) | ((uint32_t)lane << 27);
+            }
+            qtail += __popc(bal);
+            if (qtail - qhead >= 32u) {
+                process(qhead, 32u);
+                qhead += 32u;
+            }
+        }
+        if (qtail > qhead) process(qhead, qtail - qhead);
+        __syncwarp();
     }
-    own_v[warp][lane] = vi;
-    own_t[warp][lane] = __float_as_uint(pi.w);
-    const uint32_t nc = c & 0x1FFFu, ns = (c >> 13) & 0x1FFFu, fl = c >> 26;
-    const uint32_t tot = nc + ns;
-    const uint32_t maxtot = __reduce_max_sync(0xFFFFFFFFu, tot);
-    float fx = 0.f, fy = 0.f, fz = 0.f;
-    uint32_t own_lo = 0, own_hi = 0;  // my pending queue slots (bit s of lo | hi << 32)
-    uint32_t qhead = 0, qtail = 0;
-    __syncwarp();
-
-    auto process = [&](uint32_t h, uint32_t cnt) {
-        __syncwarp();
-        const uint32_t s = (h + lane) & (FQ - 1);
-        if ((uint32_t)lane < cnt) {
-            const float4 d = q_d[warp][s];
-            const uint32_t jj = q_j[warp][s];
-            const uint32_t o = jj >> 27, j = jj & 0x07FFFFFFu;
-            const float4 vo = own_v[warp][o];
-            const uint32_t tag_i = own_t[warp][o], tag_j = __float_as_uint(d.w);
-            const uint32_t sig_i = __float_as_uint(vo.w);
-            const float4 vj = __ldg(a.vel4 + j);
-            const uint32_t sig_j = __float_as_uint(vj.w);
-            const bool ifirst = tag_i < tag_j;
-            uint32_t u0 = ifirst ? sig_i : sig_j;
-            uint32_t u1 = (ifirst ? sig_j : sig_i) ^ a.step_mix;
-            tea4(u0, u1);
-            const float xi = gaussian_hot(u0, u1);
-            const float r2 = fmaf(d.x, d.x, fmaf(d.y, d.y, d.z * d.z));
-            const float rinv = rsqrt_ftz(r2);
-            const float w = fmaxf(fmaf(-r2 * rinv, a.inv_rc, 1.f), 0.f);
-            const float wr = weight_pow_f(w, a.s_exp, SMODE);
-            const float ev = (d.x * (vo.x - vj.x) + d.y * (vo.y - vj.y) + d.z * (vo.z - vj.z)) * rinv;
-            const float mag = (a.a * w - a.gamma * (wr * wr) * ev + a.sigma_dt * wr * xi) * rinv;
-            q_d[warp][s] = make_float4(mag * d.x, mag * d.y, mag * d.z, 0.f);
-        }
-        __syncwarp();
-        // owners add their slots of this window in slot (= row) order
-        uint32_t win = (h & 32u) ? own_hi : own_lo;
-        if (cnt < 32) win &= (1u << cnt) - 1u;
-        if (h & 32u)
-            own_hi &= ~win;
-        else
-            own_lo &= ~win;
-        while (win) {
-            const uint32_t b = __ffs(win) - 1;
-            const float4 fq = q_d[warp][(h + b) & (FQ - 1)];
-            fx += fq.x;
-            fy += fq.y;
-            fz += fq.z;
-            win &= win - 1;
-        }
-        __syncwarp();
-    };
-
-    // software pipeline: entries e0..e2 (positions m, m+1, m+2), position p0 (m)
-    uint32_t e0 = 0, e1 = 0, e2 = 0;
-    if (0 < tot) e0 = __ldg(a.entries + row_offset<TILED, JOINED>(i, lane, 0, nc, maxn));
-    if (1 < tot) e1 = __ldg(a.entries + row_offset<TILED, JOINED>(i, lane, 1, nc, maxn));
-    if (2 < tot) e2 = __ldg(a.entries + row_offset<TILED, JOINED>(i, lane, 2, nc, maxn));
-    float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (0 < tot) p0 = __ldg(a.pos4 + e0);
-    for (uint32_t m = 0; m < maxtot; ++m) {
-        const uint32_t j = e0;
-        const float4 pj = p0;
-        const bool act = m < tot;
-        e0 = e1;
-        e1 = e2;
-        if (m + 3 < tot) e2 = __ldg(a.entries + row_offset<TILED, JOINED>(i, lane, m + 3, nc, maxn));
-        if (m + 1 < tot) p0 = __ldg(a.pos4 + e0);
-        float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
-        if (fl) {
-            if (fl & 1u) dx = min_image_f(dx, a.L[0], a.H[0]);
-            if (fl & 2u) dy = min_image_f(dy, a.L[1], a.H[1]);
-            if (fl & 4u) dz = min_image_f(dz, a.L[2], a.H[2]);
-        }
-        const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-        bool hit = act && r2 <= a.rc2;
-        if (hit && r2 == 0.f) {
-            raise_err(a.err, DPDB_EPHYSICS, EW_COINCIDENT, __float_as_uint(pi.w),
-                      __float_as_uint(pj.w));
-            hit = false;
-        }
-        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, hit);
-        if (hit) {
-            const uint32_t s = (qtail + __popc(bal & lt)) & (FQ - 1);
-            q_d[warp][s] = make_float4(dx, dy, dz, pj.w);
-            q_j[warp][s] = j | ((uint32_t)lane << 27);
-            if (s & 32u)
-                own_hi |= 1u << (s & 31u);
+    if (coincident) raise_err(a.err, DPDB_EPHYSICS, EW_COINCIDENT, bad_tag, 0u);
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < bn; t += FORCE_WARPS * 32) {
+        const uint32_t i = b0 + t;
+        float fx = (float)acc[3 * t + 0] * FIX_INV;
+        float fy = (float)acc[3 * t + 1] * FIX_INV;
+        float fz = (float)acc[3 * t + 2] * FIX_INV;
+        if (BODY) {
+            const float g = a.xpart[i] < a.body_mid64 ? a.body_g : -a.body_g;
+            if (a.drive_axis == 0)
+                fx += g;
+            else if (a.drive_axis == 1)
+                fy += g;
             else
-                own_lo |= 1u << s;
+                fz += g;
         }
-        qtail += __popc(bal);
-        if (qtail - qhead >= 32u) {
-            process(qhead, 32u);
-            qhead += 32u;
-        }
+        a.f[0][i] = fx;
+        a.f[1][i] = fy;
+        a.f[2][i] = fz;
     }
-    if (qtail > qhead) process(qhead, qtail - qhead);
-    if (!live) return;
-    if (BODY) {
-        const float g = a.xpart[i] < a.body_mid64 ? a.body_g : -a.body_g;
-        if (a.drive_axis == 0)
-            fx += g;
-        else if (a.drive_axis == 1)
-            fy += g;
-        else
-            fz += g;
-    }
-    a.f[0][i] = fx;
-    a.f[1][i] = fy;
-    a.f[2][i] = fz;
 }
