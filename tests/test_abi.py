@@ -45,6 +45,26 @@ def test_shim_header_compiles():
     assert r.returncode == 0, r.stderr
 
 
+def build_shim_example(outdir):
+    """Compile + link tests/cpp/shim_smoke.cpp against libdpdb.so (no GPU needed)."""
+    gxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else shutil.which("g++")
+    libdir = os.path.dirname(_lib.LIB_PATH)
+    exe = os.path.join(outdir, "shim_smoke")
+    r = subprocess.run([gxx, "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "cpp", "shim_smoke.cpp"), "-L", libdir,
+                        "-ldpdb", f"-Wl,-rpath,{libdir}", "-o", exe],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_shim_example_links(tmp_path):
+    # libdpdb.so must be linkable as -ldpdb: provide the conventional soname link
+    libdir = os.path.dirname(_lib.LIB_PATH)
+    assert os.path.exists(os.path.join(libdir, "libdpdb.so"))
+    build_shim_example(str(tmp_path))
+
+
 def test_sm100a_only():
     tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
     if not os.path.exists(tool):
