@@ -49,7 +49,9 @@ struct dpdb_ctx {
     uint32_t *keys{}, *keys2{}, *vals{}, *vals2{}, *hist{};
     uint32_t *cell_start{}, *rank_of_cell{}, *stencil{};
     uint8_t *stencil_n{}, *cell_flags{};
-    uint32_t *entries{}, *counts{};
+    uint32_t *entries{}, *counts{}, *fwalk{};
+    uint2* rowmeta{};
+    bool walk = false;  // table in the builder's force-walk layout (see k_build)
     DevErr* err{};
     double *red{}, *red_out{};
     uint32_t* tmp_u32{};
@@ -324,6 +326,7 @@ int do_build(dpdb_ctx* ctx, bool joined_out) {
     if (!ctx->have_sorted) return fail(ctx, DPDB_ECONFIG, "build_neighbor_table: particles not reordered");
     ctx->tiled = true;
     ctx->joined = joined_out;
+    ctx->walk = joined_out;
     ctx->have_table = true;
     if (!ctx->n) return 0;
     dpdb::BuildArgs a{};
@@ -335,6 +338,9 @@ int do_build(dpdb_ctx* ctx, bool joined_out) {
     a.cell_flags = ctx->cell_flags;
     a.entries = ctx->entries;
     a.counts = ctx->counts;
+    a.fwalk = ctx->fwalk;
+    a.rowmeta = ctx->rowmeta;
+    a.force_block = dpdb::FORCE_BLOCK;
     a.err = ctx->err;
     a.n_local = (uint32_t)ctx->n;
     a.maxn = ctx->maxn;
@@ -369,19 +375,20 @@ int do_streams(dpdb_ctx* ctx, uint32_t* sig_out) {
     return 0;
 }
 
-template <int SMODE, bool TILED, bool JOINED>
+template <int SMODE, bool TILED, bool JOINED, bool WALK = false>
 void force_launch(dpdb_ctx* ctx, const dpdb::ForceArgs& a, bool body) {
     const unsigned nb = blocks_for(ctx->n, dpdb::FORCE_BLOCK);
     constexpr int T = dpdb::FORCE_WARPS * 32;
     if (body)
-        dpdb::k_force<SMODE, TILED, JOINED, true><<<nb, T, 0, ctx->stream>>>(a);
+        dpdb::k_force<SMODE, TILED, JOINED, true, WALK><<<nb, T, 0, ctx->stream>>>(a);
     else
-        dpdb::k_force<SMODE, TILED, JOINED, false><<<nb, T, 0, ctx->stream>>>(a);
+        dpdb::k_force<SMODE, TILED, JOINED, false, WALK><<<nb, T, 0, ctx->stream>>>(a);
 }
 
 template <int SMODE>
 void force_dispatch_layout(dpdb_ctx* ctx, const dpdb::ForceArgs& a, bool body) {
-    if (ctx->tiled && !ctx->joined) force_launch<SMODE, true, false>(ctx, a, body);
+    if (ctx->walk) force_launch<SMODE, true, true, true>(ctx, a, body);
+    else if (ctx->tiled && !ctx->joined) force_launch<SMODE, true, false>(ctx, a, body);
     else if (ctx->tiled) force_launch<SMODE, true, true>(ctx, a, body);
     else if (!ctx->joined) force_launch<SMODE, false, false>(ctx, a, body);
     else force_launch<SMODE, false, true>(ctx, a, body);
@@ -396,6 +403,7 @@ int do_forces(dpdb_ctx* ctx, uint32_t step) {
     a.vel4 = ctx->vel4;
     a.entries = ctx->entries;
     a.counts = ctx->counts;
+    a.fwalk = ctx->fwalk;
     a.xpart = ctx->x[ctx->run.partition_axis];
     for (int k = 0; k < 3; ++k) a.f[k] = ctx->f[k];
     a.err = ctx->err;
@@ -570,6 +578,7 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         (rc = dalloc(ctx, ctx->stencil_n, (size_t)g.n_local_cells)) ||
         (rc = dalloc(ctx, ctx->cell_flags, (size_t)g.n_local_cells)) ||
         (rc = dalloc(ctx, ctx->entries, c * ctx->maxn)) || (rc = dalloc(ctx, ctx->counts, c)) ||
+        (rc = dalloc(ctx, ctx->fwalk, c)) || (rc = dalloc(ctx, ctx->rowmeta, c)) ||
         (rc = dalloc(ctx, ctx->err, 1)) || (rc = dalloc(ctx, ctx->red, (size_t)RED_BLOCKS * 4)) ||
         (rc = dalloc(ctx, ctx->red_out, 8)) || (rc = dalloc(ctx, ctx->tmp_u32, c)))
         return bail(rc);
@@ -605,7 +614,8 @@ int dpdb_destroy(dpdb_ctx* ctx) {
     void* ptrs[] = {ctx->tag, ctx->tag2, ctx->mol, ctx->mol2, ctx->sp, ctx->sp2, ctx->pos4,
                     ctx->vel4, ctx->keys, ctx->keys2, ctx->vals, ctx->vals2, ctx->hist,
                     ctx->cell_start, ctx->rank_of_cell, ctx->stencil, ctx->stencil_n,
-                    ctx->cell_flags, ctx->entries, ctx->counts, ctx->err, ctx->red, ctx->red_out,
+                    ctx->cell_flags, ctx->entries, ctx->counts, ctx->fwalk, ctx->rowmeta,
+                    ctx->err, ctx->red, ctx->red_out,
                     ctx->tmp_u32, ctx->bond_off, ctx->bond_partner, ctx->index_of_tag,
                     ctx->bond_k, ctx->bond_r0};
     for (void* p : ptrs)
@@ -861,9 +871,46 @@ int dpdb_build_neighbors(dpdb_ctx* ctx) {
     return check_device(ctx);
 }
 
+namespace {
+// Restore the reference's joined rows (core ascending, skin ascending) from the
+// builder's force-walk layout using rowmeta (c1, c2, s1, s2; see k_build):
+// walk order = core[0,c1) core[c2,nc) skin[0,s1) skin[s2,ns) core[c1,c2) skin[s1,s2).
+int unwalk(dpdb_ctx* ctx) {
+    if (!ctx->walk) return 0;
+    const size_t n = ctx->n, rows = (n + 31) & ~(size_t)31, maxn = ctx->maxn;
+    ctx->walk = false;
+    if (!rows) return 0;
+    std::vector<uint32_t> raw(rows * maxn), cnt(n), out(rows * maxn, 0u);
+    std::vector<uint2> meta(n);
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(raw.data(), ctx->entries, raw.size() * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(cnt.data(), ctx->counts, n * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(meta.data(), ctx->rowmeta, n * sizeof(uint2), cudaMemcpyDeviceToHost));
+    auto idx = [&](size_t i, size_t k) { return ((i & ~size_t(31)) + (k & 31)) * maxn + (k & ~size_t(31)) + (i & 31); };
+    std::vector<uint32_t> row(maxn);
+    for (size_t i = 0; i < n; ++i) {
+        const uint32_t nc = cnt[i] & 0x1FFFu, ns = (cnt[i] >> 13) & 0x1FFFu;
+        const uint32_t c1 = meta[i].x & 0xFFFFu, c2 = meta[i].x >> 16;
+        const uint32_t s1 = meta[i].y & 0xFFFFu, s2 = meta[i].y >> 16;
+        const uint32_t A = c1, B = A + (nc - c2), C = B + s1, D = C + (ns - s2), E = D + (c2 - c1);
+        uint32_t w = 0;
+        for (uint32_t k = 0; k < A; ++k) row[w++] = raw[idx(i, k)];
+        for (uint32_t k = D; k < E; ++k) row[w++] = raw[idx(i, k)];
+        for (uint32_t k = A; k < B; ++k) row[w++] = raw[idx(i, k)];
+        for (uint32_t k = B; k < C; ++k) row[w++] = raw[idx(i, k)];
+        for (uint32_t k = E; k < nc + ns; ++k) row[w++] = raw[idx(i, k)];
+        for (uint32_t k = C; k < D; ++k) row[w++] = raw[idx(i, k)];
+        for (uint32_t k = 0; k < w; ++k) out[idx(i, k)] = row[k];
+    }
+    CK(cudaMemcpy(ctx->entries, out.data(), out.size() * 4, cudaMemcpyHostToDevice));
+    return 0;
+}
+}  // namespace
+
 int dpdb_join_core_skin(dpdb_ctx* ctx) {
     TRY(require_ctx(ctx));
     if (!ctx->have_table) return fail(ctx, DPDB_ECONFIG, "join_core_skin: no table");
+    TRY(unwalk(ctx));
     if (ctx->joined) return 0;
     if (ctx->n) {
         dpdb::k_join<<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(ctx->entries, ctx->counts,
@@ -878,6 +925,7 @@ int dpdb_join_core_skin(dpdb_ctx* ctx) {
 int dpdb_tile_transpose(dpdb_ctx* ctx) {
     TRY(require_ctx(ctx));
     if (!ctx->have_table) return fail(ctx, DPDB_ECONFIG, "tile_transpose: no table");
+    TRY(unwalk(ctx));
     const uint32_t rows = (uint32_t)((ctx->n + 31) & ~(size_t)31);
     if (rows) {
         dim3 grid(ctx->maxn / 32, rows / 32), blk(32, 8);
@@ -892,6 +940,7 @@ int dpdb_get_neighbors(dpdb_ctx* ctx, uint32_t* entries, uint16_t* core, uint16_
                        int32_t* tiled, int32_t* joined) {
     TRY(require_ctx(ctx));
     if (!ctx->have_table) return fail(ctx, DPDB_ECONFIG, "get_neighbors: no table");
+    TRY(unwalk(ctx));
     const size_t n = ctx->n, rows = (n + 31) & ~(size_t)31, maxn = ctx->maxn;
     std::vector<uint32_t> cnt(n);
     CK(cudaMemcpy(cnt.data(), ctx->counts, n * 4, cudaMemcpyDeviceToHost));

@@ -10,6 +10,7 @@ struct ForceArgs {
     const float4* vel4;
     const uint32_t* entries;
     const uint32_t* counts;
+    const uint32_t* fwalk;  // walk layout only: n_eval | flags << 26
     const double* xpart;  // fp64 coordinate on the partition axis (body force)
     float* f[3];
     DevErr* err;
@@ -111,7 +112,11 @@ __device__ __forceinline__ uint32_t row_offset(uint32_t lane, uint32_t m, uint32
 // added as +q to i and -q to j in the block accumulator.  Deterministic run
 // to run, and Newton's third law holds exactly.  Row entries and candidate
 // positions are software-pipelined (entries 3 ahead, positions 1 ahead).
-template <int SMODE, bool TILED, bool JOINED, bool BODY>
+//
+// WALK: the table is in the builder's walk layout (k_build<..., true>): each
+// row lists first the entries this particle evaluates and n_eval = fwalk & 0x1FFF,
+// so the in-block j < i entries are never loaded.
+template <int SMODE, bool TILED, bool JOINED, bool BODY, bool WALK>
 __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(ForceArgs a) {
     __shared__ float4 q_d[FORCE_WARPS][FQ];   // (dx, dy, dz, tag_j)
     __shared__ uint32_t q_j[FORCE_WARPS][FQ]; // j | in_block << 26 | owner lane << 27
@@ -139,11 +144,11 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(ForceArgs a) {
         if (live) {
             pi = a.pos4[i];
             vi = a.vel4[i];
-            c = a.counts[i];
+            c = WALK ? a.fwalk[i] : a.counts[i];
         }
         own_v[warp][lane] = vi;
-        const uint32_t nc = c & 0x1FFFu, ns = (c >> 13) & 0x1FFFu, fl = c >> 26;
-        const uint32_t tot = nc + ns;
+        const uint32_t nc = WALK ? 0u : c & 0x1FFFu, fl = c >> 26;
+        const uint32_t tot = WALK ? (c & 0x1FFFu) : nc + ((c >> 13) & 0x1FFFu);
         const uint32_t maxtot = __reduce_max_sync(0xFFFFFFFFu, tot);
         const uint32_t tag_me = __float_as_uint(pi.w);
         own_t[warp][lane] = tag_me;
@@ -195,9 +200,10 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(ForceArgs a) {
         // software pipeline: entries e0..e2 (positions m, m+1, m+2), position p0 (m)
         const uint32_t* erow = a.entries + (size_t)(b0 + il0) * maxn + lane;
         uint32_t e0 = 0, e1 = 0, e2 = 0;
-        if (0 < tot) e0 = __ldg(erow + row_offset<TILED, JOINED>(lane, 0, nc, maxn));
-        if (1 < tot) e1 = __ldg(erow + row_offset<TILED, JOINED>(lane, 1, nc, maxn));
-        if (2 < tot) e2 = __ldg(erow + row_offset<TILED, JOINED>(lane, 2, nc, maxn));
+        constexpr bool JN = JOINED || WALK;
+        if (0 < tot) e0 = __ldg(erow + row_offset<TILED, JN>(lane, 0, nc, maxn));
+        if (1 < tot) e1 = __ldg(erow + row_offset<TILED, JN>(lane, 1, nc, maxn));
+        if (2 < tot) e2 = __ldg(erow + row_offset<TILED, JN>(lane, 2, nc, maxn));
         float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f);
         if (0 < tot) p0 = __ldg(a.pos4 + e0);
         for (uint32_t m = 0; m < maxtot; ++m) {
@@ -205,10 +211,10 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(ForceArgs a) {
             const float4 pj = p0;
             const uint32_t jl = j - b0;
             const bool inblk = jl < bn;
-            const bool act = m < tot && !(inblk && jl < il);  // lower index takes the pair
+            const bool act = m < tot && (WALK || !(inblk && jl < il));  // lower index takes it
             e0 = e1;
             e1 = e2;
-            if (m + 3 < tot) e2 = __ldg(erow + row_offset<TILED, JOINED>(lane, m + 3, nc, maxn));
+            if (m + 3 < tot) e2 = __ldg(erow + row_offset<TILED, JN>(lane, m + 3, nc, maxn));
             if (m + 1 < tot) p0 = __ldg(a.pos4 + e0);
             float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
             if (fl) {

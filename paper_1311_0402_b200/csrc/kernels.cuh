@@ -429,8 +429,11 @@ struct BuildArgs {
     const uint8_t* cell_flags;
     uint32_t* entries;
     uint32_t* counts;
+    uint32_t* fwalk;    // walk layout: n_eval | force-wrap-flags << 26
+    uint2* rowmeta;     // walk layout: (c1 | c2 << 16, s1 | s2 << 16)
     DevErr* err;
     uint32_t n_local, maxn, n_local_cells;
+    uint32_t force_block;  // power of two
     int key_shift;
     float cut_c, cut_s;
     float L[3], H[3];
@@ -579,14 +582,51 @@ __global__ void __launch_bounds__(WARPS * 32) k_build(BuildArgs a) {
         const uint32_t maxc = __reduce_max_sync(0xFFFFFFFFu, min(nc, maxn));
         const uint32_t maxs = __reduce_max_sync(0xFFFFFFFFu, min(nsk, maxn));
         uint32_t* tb = a.entries + (size_t)ti0 * maxn + lane;
+        uint32_t n_eval = 0;
         if (JOINED_OUT) {
-            // join_core_skin folded in: core ascending then skin ascending
-            const uint32_t nt = min(nc + nsk, maxn);
+            // Walk order for the force kernel (join_core_skin folded in):
+            // the entries the force kernel evaluates first -- j outside this
+            // particle's force block, or j > i -- core then skin, each ascending;
+            // then the in-block j < i entries (that pair is taken by j).  With
+            // rowmeta the exact ascending rows are recovered for export.
+            const uint32_t ncc = min(nc, maxn), nss = min(nsk, maxn - ncc);
+            const uint32_t fb0 = i & ~(a.force_block - 1u);
+            auto lower = [&](uint32_t v, bool skin, uint32_t cnt) {  // #entries < v
+                uint32_t lo = 0, hi = cnt;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    const uint32_t r = skin ? maxn - 1u - mid : mid;
+                    if (buf[r * STRIDE + col] < v)
+                        lo = mid + 1;
+                    else
+                        hi = mid;
+                }
+                return lo;
+            };
+            const uint32_t c1 = lower(fb0, false, ncc), c2 = lower(i, false, ncc);
+            const uint32_t s1 = lower(fb0, true, nss), s2 = lower(i, true, nss);
+            const uint32_t A = c1, B = A + (ncc - c2), Cq = B + s1, D = Cq + (nss - s2);
+            const uint32_t E = D + (c2 - c1);
+            n_eval = D;
+            const uint32_t nt = ncc + nss;
             const uint32_t maxt = __reduce_max_sync(0xFFFFFFFFu, nt);
             for (uint32_t k = 0; k < maxt; ++k) {
-                const uint32_t src = k < nc ? k : maxn - 1u - (k - nc);
+                uint32_t src;
+                if (k < A)
+                    src = k;
+                else if (k < B)
+                    src = c2 + (k - A);
+                else if (k < Cq)
+                    src = maxn - 1u - (k - B);
+                else if (k < D)
+                    src = maxn - 1u - (s2 + (k - Cq));
+                else if (k < E)
+                    src = c1 + (k - D);
+                else
+                    src = maxn - 1u - (s1 + (k - E));
                 tb[(k & 31u) * maxn + (k & ~31u)] = k < nt ? buf[src * STRIDE + col] : 0u;
             }
+            if (row) a.rowmeta[i] = make_uint2(c1 | (c2 << 16), s1 | (s2 << 16));
         } else {
             for (uint32_t k = 0; k < maxc; ++k)
                 tb[(k & 31u) * maxn + (k & ~31u)] = k < nc ? buf[k * STRIDE + col] : 0u;
@@ -598,6 +638,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_build(BuildArgs a) {
         if (row) {
             const uint32_t ff = (a.cell_flags[min(a.keys[i] >> a.key_shift, rl)] >> 3) & 7u;
             a.counts[i] = min(nc, 8191u) | (min(nsk, 8191u) << 13) | (ff << 26);
+            if (JOINED_OUT) a.fwalk[i] = n_eval | (ff << 26);
         }
     }
 }

@@ -98,6 +98,27 @@ def test_join_and_transpose_device():
     assert e.neighbor_table().tiled
 
 
+def test_pipeline_walk_layout_exports_reference_rows():
+    """dpdb_setup builds the force-walk layout (half-list order); the export
+    restores the reference's joined ascending rows exactly."""
+    maxn = 128
+    box, obox, st = _sys.fluid((14, 14, 14), 3.0, seed=9)
+    e = _sys.engine(box, st)
+    e.setup()
+    f_walk = np.stack(e.download().force, 1)
+    t = e.neighbor_table()
+    assert t.joined and t.tiled
+    E, core, skin, s = oracle_table(obox, st, maxn)
+    assert np.array_equal(t.core_count, core[: t.n_rows]) and np.array_equal(t.skin_count, skin[: t.n_rows])
+    for i in range(t.n_rows):
+        assert np.array_equal(t.core_row(i), E[i, : core[i]])
+        assert np.array_equal(t.skin_row(i), E[i, maxn - skin[i]:][::-1])
+    # forces from the restored layout (WALK=false path) equal the walk-layout forces
+    e.compute_forces(0)
+    f_joined = np.stack(e.download().force, 1)
+    assert np.array_equal(f_walk, f_joined)
+
+
 def test_overflow_is_physics_error():
     box, obox, st = _sys.fluid((4.0, 4.0, 4.0), 50, seed=3)
     e = _sys.engine(box, st, run=dpd.RunConfig(max_neighbors=128))
