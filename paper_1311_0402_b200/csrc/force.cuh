@@ -79,6 +79,9 @@ constexpr int FORCE_WARPS = 8;   // warps per CTA
 constexpr int FORCE_TILES = 16;  // 32-row tiles per CTA block: B = 512 particles
 constexpr int FORCE_BLOCK = 32 * FORCE_TILES;
 constexpr int FQ = 64;  // per-warp pair queue (slots)
+#ifndef FORCE_MIN_BLOCKS
+#define FORCE_MIN_BLOCKS 5  // 48 registers: measured best (4 -> 0.61 ms, 6 -> 0.53 ms, 5 -> 0.52 ms)
+#endif
 // Forces are accumulated as 2^-18 fixed-point int32 (|F| < 8192 per particle,
 // resolution 3.8e-6): integer sums commute, so the result does not depend on
 // the order in which lanes or warps deliver their shares.
@@ -117,23 +120,27 @@ __device__ __forceinline__ uint32_t row_offset(uint32_t lane, uint32_t m, uint32
 // row lists first the entries this particle evaluates and n_eval = fwalk & 0x1FFF,
 // so the in-block j < i entries are never loaded.
 template <int SMODE, bool TILED, bool JOINED, bool BODY, bool WALK>
-__global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(ForceArgs a) {
+__global__ void __launch_bounds__(FORCE_WARPS * 32, FORCE_MIN_BLOCKS) k_force(ForceArgs a) {
     __shared__ float4 q_d[FORCE_WARPS][FQ];   // (dx, dy, dz, tag_j)
     __shared__ uint32_t q_j[FORCE_WARPS][FQ]; // j | in_block << 26 | owner lane << 27
     __shared__ float4 own_v[FORCE_WARPS][32];
     __shared__ uint32_t own_t[FORCE_WARPS][32];
     __shared__ int acc[FORCE_BLOCK * 3];
+    __shared__ uint32_t next_tile;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t b0 = blockIdx.x * FORCE_BLOCK;
     const uint32_t bn = min((uint32_t)FORCE_BLOCK, a.n - b0);  // particles in this block
     for (int t = threadIdx.x; t < FORCE_BLOCK * 3; t += FORCE_WARPS * 32) acc[t] = 0;
+    if (threadIdx.x == 0) next_tile = FORCE_WARPS;
     __syncthreads();
     const uint32_t lt = lanemask_lt();
     const uint32_t maxn = a.maxn;
     bool coincident = false;
     uint32_t bad_tag = 0;
 
-    for (int tile = warp; tile < FORCE_TILES; tile += FORCE_WARPS) {
+    // tiles are handed out dynamically: rows differ in length, so a static
+    // round-robin leaves warps idle at the final barrier
+    for (uint32_t tile = warp; tile < FORCE_TILES;) {
         const uint32_t il0 = 32u * tile;
         if (il0 >= bn) break;
         const uint32_t il = il0 + lane;  // my index in the block
@@ -241,7 +248,9 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(ForceArgs a) {
             }
         }
         if (qtail > qhead) process(qhead, qtail - qhead);
-        __syncwarp();
+        uint32_t nt = 0;
+        if (lane == 0) nt = atomicAdd(&next_tile, 1u);
+        tile = __shfl_sync(0xFFFFFFFFu, nt, 0);
     }
     if (coincident) raise_err(a.err, DPDB_EPHYSICS, EW_COINCIDENT, bad_tag, 0u);
     __syncthreads();
