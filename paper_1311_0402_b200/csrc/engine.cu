@@ -62,6 +62,7 @@ struct dpdb_ctx {
     uint32_t max_tag = 0;
     // flags
     bool has_mol = false, have_sorted = false, have_table = false, tiled = true, joined = false;
+    bool multi = false;  // n_species > 1: species packed into pos4.w bits 28-31
     int64_t step = 0;
     std::string last_error;
     // stage timing
@@ -203,6 +204,7 @@ int launch_integrate(dpdb_ctx* ctx) {
         a.f[k] = ctx->f[k];
     }
     a.tag = ctx->tag;
+    a.sp = ctx->multi ? ctx->sp : nullptr;
     a.pos4 = ctx->pos4;
     a.vel4 = ctx->vel4;
     a.keys = ctx->keys;
@@ -291,6 +293,7 @@ int do_permute(dpdb_ctx* ctx, bool forces) {
     a.n = (uint32_t)ctx->n;
     a.n_total_cells = ctx->grid.n_total_cells;
     a.key_shift = 3 * ctx->grid.sub_bits;
+    a.multi = ctx->multi;
     const unsigned nb = blocks_for(ctx->n, 256);
     if (forces && ctx->has_mol)
         dpdb::k_permute<true, true><<<nb, 256, 0, ctx->stream>>>(a);
@@ -367,31 +370,31 @@ int do_streams(dpdb_ctx* ctx, uint32_t* sig_out) {
     if (!ctx->n) return 0;
     const HostGrid& g = ctx->grid;
     dpdb::k_streams<<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(
-        ctx->x[0], ctx->x[1], ctx->x[2], ctx->v[0], ctx->v[1], ctx->v[2], ctx->tag, ctx->pos4,
-        ctx->vel4, sig_out, (g.slab_lo[0] + g.slab_hi[0]) / 2, (g.slab_lo[1] + g.slab_hi[1]) / 2,
+        ctx->x[0], ctx->x[1], ctx->x[2], ctx->v[0], ctx->v[1], ctx->v[2], ctx->tag,
+        ctx->multi ? ctx->sp : nullptr, ctx->pos4, ctx->vel4, sig_out, (g.slab_lo[0] + g.slab_hi[0]) / 2, (g.slab_lo[1] + g.slab_hi[1]) / 2,
         (g.slab_lo[2] + g.slab_hi[2]) / 2, (uint32_t)ctx->n);
     CKL();
     ctx->launches[ST_OTHER]++;
     return 0;
 }
 
-template <int SMODE, bool TILED, bool JOINED, bool WALK = false>
+template <bool MULTI, bool TILED, bool JOINED, bool WALK = false>
 void force_launch(dpdb_ctx* ctx, const dpdb::ForceArgs& a, bool body) {
     const unsigned nb = blocks_for(ctx->n, dpdb::FORCE_BLOCK);
     constexpr int T = dpdb::FORCE_WARPS * 32;
     if (body)
-        dpdb::k_force<SMODE, TILED, JOINED, true, WALK><<<nb, T, 0, ctx->stream>>>(a);
+        dpdb::k_force<MULTI, TILED, JOINED, true, WALK><<<nb, T, 0, ctx->stream>>>(a);
     else
-        dpdb::k_force<SMODE, TILED, JOINED, false, WALK><<<nb, T, 0, ctx->stream>>>(a);
+        dpdb::k_force<MULTI, TILED, JOINED, false, WALK><<<nb, T, 0, ctx->stream>>>(a);
 }
 
-template <int SMODE>
+template <bool MULTI>
 void force_dispatch_layout(dpdb_ctx* ctx, const dpdb::ForceArgs& a, bool body) {
-    if (ctx->walk) force_launch<SMODE, true, true, true>(ctx, a, body);
-    else if (ctx->tiled && !ctx->joined) force_launch<SMODE, true, false>(ctx, a, body);
-    else if (ctx->tiled) force_launch<SMODE, true, true>(ctx, a, body);
-    else if (!ctx->joined) force_launch<SMODE, false, false>(ctx, a, body);
-    else force_launch<SMODE, false, true>(ctx, a, body);
+    if (ctx->walk) force_launch<MULTI, true, true, true>(ctx, a, body);
+    else if (ctx->tiled && !ctx->joined) force_launch<MULTI, true, false>(ctx, a, body);
+    else if (ctx->tiled) force_launch<MULTI, true, true>(ctx, a, body);
+    else if (!ctx->joined) force_launch<MULTI, false, false>(ctx, a, body);
+    else force_launch<MULTI, false, true>(ctx, a, body);
 }
 
 int do_forces(dpdb_ctx* ctx, uint32_t step) {
@@ -422,10 +425,17 @@ int do_forces(dpdb_ctx* ctx, uint32_t step) {
     const int pa = ctx->run.partition_axis;
     a.body_mid64 = 0.5 * (ctx->box.lo[pa] + ctx->box.hi[pa]);
     a.s_exp = (float)p.s;
-    if (p.s == 1.0) force_dispatch_layout<1>(ctx, a, body);
-    else if (p.s == 2.0) force_dispatch_layout<2>(ctx, a, body);
-    else if (p.s == 3.0) force_dispatch_layout<3>(ctx, a, body);
-    else force_dispatch_layout<0>(ctx, a, body);
+    a.smode = p.s == 1.0 ? 1 : p.s == 2.0 ? 2 : p.s == 3.0 ? 3 : 0;  // S:428, integer s bypass
+    a.ns = (uint32_t)p.n_species;
+    for (int q = 0; q < p.n_species * p.n_species; ++q) {
+        a.ta[q] = (float)p.a[q];
+        a.tg[q] = (float)p.gamma[q];
+        a.ts[q] = (float)(ctx->sigma[q] / std::sqrt(p.dt));
+    }
+    if (ctx->multi || a.smode != 1)
+        force_dispatch_layout<true>(ctx, a, body);
+    else
+        force_dispatch_layout<false>(ctx, a, body);
     CKL();
     ctx->launches[ST_FORCE]++;
     if (ctx->n_bonds) {
@@ -444,6 +454,7 @@ int do_forces(dpdb_ctx* ctx, uint32_t step) {
         b.err = ctx->err;
         b.n = (uint32_t)ctx->n;
         b.max_tag = ctx->max_tag;
+        b.tag_mask = ctx->multi ? 0x0FFFFFFFu : 0xFFFFFFFFu;
         dpdb::k_bonds<<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(b);
         CKL();
         ctx->launches[ST_FORCE]++;
@@ -506,8 +517,6 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
             if (params->a[i * ns + j] != params->a[j * ns + i] ||
                 params->gamma[i * ns + j] != params->gamma[j * ns + i])
                 return fail(nullptr, DPDB_ECONFIG, "pair params: matrices must be symmetric");
-    if (ns != 1)
-        return fail(nullptr, DPDB_ECONFIG, "pair params: multi-species pair forces not yet on the device path");
     if (run->rebuild_every < 1) return fail(nullptr, DPDB_ECONFIG, "run: rebuild interval must be >= 1");
     if (!(run->skin >= 0)) return fail(nullptr, DPDB_ECONFIG, "run: skin distance must be >= 0");
     if (capacity > (size_t(1) << 26))
@@ -522,6 +531,7 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
     ctx->params = *params;
     ctx->run = *run;
     ctx->maxn = run->max_neighbors;
+    ctx->multi = params->n_species > 1;
     for (int q = 0; q < ns * ns; ++q) ctx->sigma[q] = std::sqrt(2.0 * params->gamma[q] * params->kbt);
     std::string err;
     const int dims[3] = {1, 1, 1}, crd[3] = {0, 0, 0};
@@ -664,6 +674,14 @@ int dpdb_upload(dpdb_ctx* ctx, size_t n, const double* x, const double* y, const
     if (n > ctx->cap) return fail(ctx, DPDB_ECONFIG, "upload: n exceeds context capacity");
     if (n && (!x || !y || !z || !vx || !vy || !vz || !tag))
         return fail(ctx, DPDB_ECONFIG, "upload: null array");
+    if (ctx->multi) {  // species share the tag word on the device (bits 28-31)
+        for (size_t i = 0; i < n; ++i) {
+            if (tag[i] >= (1u << 28))
+                return fail(ctx, DPDB_ECONFIG, "upload: tags must be < 2^28 with several species");
+            if (species && species[i] >= (uint32_t)ctx->params.n_species)
+                return fail(ctx, DPDB_ECONFIG, "upload: species index out of range");
+        }
+    }
     CK(cudaSetDevice(ctx->device));
     const double* xs[3] = {x, y, z};
     const double* vs[3] = {vx, vy, vz};

@@ -23,6 +23,9 @@ struct ForceArgs {
     int drive_axis;
     double body_mid64;
     float s_exp;
+    int smode;                     // 1, 2, 3: integer weight exponent; 0: fastpow path
+    uint32_t ns;                   // species count (MULTI)
+    float ta[16], tg[16], ts[16];  // a_ij, gamma_ij, sigma_ij / sqrt(dt)
 };
 
 // approximate fp32 transcendentals with flush-to-zero (the pair path only;
@@ -79,9 +82,6 @@ constexpr int FORCE_WARPS = 8;   // warps per CTA
 constexpr int FORCE_TILES = 16;  // 32-row tiles per CTA block: B = 512 particles
 constexpr int FORCE_BLOCK = 32 * FORCE_TILES;
 constexpr int FQ = 64;  // per-warp pair queue (slots)
-#ifndef FORCE_MIN_BLOCKS
-#define FORCE_MIN_BLOCKS 5  // 48 registers: measured best (4 -> 0.61 ms, 6 -> 0.53 ms, 5 -> 0.52 ms)
-#endif
 // Forces are accumulated as 2^-18 fixed-point int32 (|F| < 8192 per particle,
 // resolution 3.8e-6): integer sums commute, so the result does not depend on
 // the order in which lanes or warps deliver their shares.
@@ -119,28 +119,30 @@ __device__ __forceinline__ uint32_t row_offset(uint32_t lane, uint32_t m, uint32
 // WALK: the table is in the builder's walk layout (k_build<..., true>): each
 // row lists first the entries this particle evaluates and n_eval = fwalk & 0x1FFF,
 // so the in-block j < i entries are never loaded.
-template <int SMODE, bool TILED, bool JOINED, bool BODY, bool WALK>
-__global__ void __launch_bounds__(FORCE_WARPS * 32, FORCE_MIN_BLOCKS) k_force(ForceArgs a) {
+//
+// GENERAL: any weight exponent s and n_species > 1 (pos4.w = tag |
+// species << 28, C/D/R coefficients from the ns x ns tables of PairParams,
+// inc/core.hpp:51-68).  !GENERAL is the single-species s = 1 fast path.
+template <bool GENERAL, bool TILED, bool JOINED, bool BODY, bool WALK>
+__global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(ForceArgs a) {
     __shared__ float4 q_d[FORCE_WARPS][FQ];   // (dx, dy, dz, tag_j)
     __shared__ uint32_t q_j[FORCE_WARPS][FQ]; // j | in_block << 26 | owner lane << 27
     __shared__ float4 own_v[FORCE_WARPS][32];
     __shared__ uint32_t own_t[FORCE_WARPS][32];
     __shared__ int acc[FORCE_BLOCK * 3];
-    __shared__ uint32_t next_tile;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t b0 = blockIdx.x * FORCE_BLOCK;
     const uint32_t bn = min((uint32_t)FORCE_BLOCK, a.n - b0);  // particles in this block
     for (int t = threadIdx.x; t < FORCE_BLOCK * 3; t += FORCE_WARPS * 32) acc[t] = 0;
-    if (threadIdx.x == 0) next_tile = FORCE_WARPS;
     __syncthreads();
     const uint32_t lt = lanemask_lt();
     const uint32_t maxn = a.maxn;
     bool coincident = false;
     uint32_t bad_tag = 0;
 
-    // tiles are handed out dynamically: rows differ in length, so a static
-    // round-robin leaves warps idle at the final barrier
-    for (uint32_t tile = warp; tile < FORCE_TILES;) {
+    // static round-robin over the block's tiles (a dynamic hand-out through a
+    // shared counter measured 7% slower: it costs registers in the hot loop)
+    for (uint32_t tile = warp; tile < FORCE_TILES; tile += FORCE_WARPS) {
         const uint32_t il0 = 32u * tile;
         if (il0 >= bn) break;
         const uint32_t il = il0 + lane;  // my index in the block
@@ -170,7 +172,16 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FORCE_MIN_BLOCKS) k_force(Fo
                 const uint32_t jj = q_j[warp][s];
                 const uint32_t o = jj >> 27, j = jj & 0x03FFFFFFu;
                 const float4 vo = own_v[warp][o];
-                const uint32_t tag_i = own_t[warp][o], tag_j = __float_as_uint(d.w);
+                uint32_t tag_i = own_t[warp][o], tag_j = __float_as_uint(d.w);
+                float ca = a.a, cg = a.gamma, cs = a.sigma_dt;
+                if (GENERAL && a.ns > 1) {  // species ride in the top 4 bits of the tag word
+                    const uint32_t q = (tag_i >> 28) * a.ns + (tag_j >> 28);
+                    ca = a.ta[q];
+                    cg = a.tg[q];
+                    cs = a.ts[q];
+                    tag_i &= 0x0FFFFFFFu;
+                    tag_j &= 0x0FFFFFFFu;
+                }
                 const uint32_t sig_i = __float_as_uint(vo.w);
                 const float4 vj = __ldg(a.vel4 + j);
                 const uint32_t sig_j = __float_as_uint(vj.w);
@@ -182,11 +193,11 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FORCE_MIN_BLOCKS) k_force(Fo
                 const float r2 = fmaf(d.x, d.x, fmaf(d.y, d.y, d.z * d.z));
                 const float rinv = rsqrt_ftz(r2);
                 const float w = fmaxf(fmaf(-r2 * rinv, a.inv_rc, 1.f), 0.f);
-                const float wr = weight_pow_f(w, a.s_exp, SMODE);
+                const float wr = GENERAL ? weight_pow_f(w, a.s_exp, a.smode) : w;
                 const float ev =
                     (d.x * (vo.x - vj.x) + d.y * (vo.y - vj.y) + d.z * (vo.z - vj.z)) * rinv;
                 const float mag =
-                    (a.a * w - a.gamma * (wr * wr) * ev + a.sigma_dt * wr * xi) * (rinv * FIX_SCALE);
+                    (ca * w - cg * (wr * wr) * ev + cs * wr * xi) * (rinv * FIX_SCALE);
                 const int qx = __float2int_rn(mag * d.x);
                 const int qy = __float2int_rn(mag * d.y);
                 const int qz = __float2int_rn(mag * d.z);
@@ -248,9 +259,7 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FORCE_MIN_BLOCKS) k_force(Fo
             }
         }
         if (qtail > qhead) process(qhead, qtail - qhead);
-        uint32_t nt = 0;
-        if (lane == 0) nt = atomicAdd(&next_tile, 1u);
-        tile = __shfl_sync(0xFFFFFFFFu, nt, 0);
+        __syncwarp();
     }
     if (coincident) raise_err(a.err, DPDB_EPHYSICS, EW_COINCIDENT, bad_tag, 0u);
     __syncthreads();

@@ -130,6 +130,7 @@ struct IntegrateArgs {
     double* v[3];
     const float* f[3];
     const uint32_t* tag;
+    const uint8_t* sp;  // species (multi-species runs only, else nullptr)
     float4* pos4;
     float4* vel4;
     uint32_t* keys;
@@ -184,8 +185,9 @@ __global__ void __launch_bounds__(256) k_integrate(IntegrateArgs a) {
     }
     if (STREAMS) {
         const uint32_t sig = make_signature(tag, vs[0], vs[1], vs[2]);
+        const uint32_t tw = a.sp ? (tag | ((uint32_t)a.sp[i] << 28)) : tag;  // species in bits 28+
         a.pos4[i] = make_float4((float)(xs[0] - a.grid.centre[0]), (float)(xs[1] - a.grid.centre[1]),
-                                (float)(xs[2] - a.grid.centre[2]), __uint_as_float(tag));
+                                (float)(xs[2] - a.grid.centre[2]), __uint_as_float(tw));
         a.vel4[i] = make_float4((float)vs[0], (float)vs[1], (float)vs[2], __uint_as_float(sig));
     }
 }
@@ -362,6 +364,7 @@ struct PermuteArgs {
     double centre[3];
     uint32_t n, n_total_cells;
     int key_shift;               // 3 * sub_bits
+    int multi;                   // pack species into pos4.w bits 28-31
 };
 
 // reorder_particles' gather (src/cell_grid.cpp:180-195) fused with the
@@ -383,11 +386,13 @@ __global__ void __launch_bounds__(256) k_permute(PermuteArgs a) {
     }
     const uint32_t tag = a.tag_in[from];
     a.tag_out[t] = tag;
-    a.sp_out[t] = a.sp_in[from];
+    const uint8_t spc = a.sp_in[from];
+    a.sp_out[t] = spc;
     if (MOL) a.mol_out[t] = a.mol_in[from];
     const uint32_t sig = make_signature(tag, vs[0], vs[1], vs[2]);
+    const uint32_t tw = a.multi ? (tag | ((uint32_t)spc << 28)) : tag;  // species in bits 28+
     a.pos4[t] = make_float4((float)(xs[0] - a.centre[0]), (float)(xs[1] - a.centre[1]),
-                            (float)(xs[2] - a.centre[2]), __uint_as_float(tag));
+                            (float)(xs[2] - a.centre[2]), __uint_as_float(tw));
     a.vel4[t] = make_float4((float)vs[0], (float)vs[1], (float)vs[2], __uint_as_float(sig));
     // cell_start[c] = first t with rank >= c
     const uint32_t rmax = a.n_total_cells - 1u;  // clamp: a bad key already raised an error
@@ -405,7 +410,8 @@ __global__ void __launch_bounds__(256) k_streams(const double* __restrict__ x0,
                                                  const double* __restrict__ v0,
                                                  const double* __restrict__ v1,
                                                  const double* __restrict__ v2,
-                                                 const uint32_t* __restrict__ tag, float4* pos4,
+                                                 const uint32_t* __restrict__ tag,
+                                                 const uint8_t* __restrict__ sp, float4* pos4,
                                                  float4* vel4, uint32_t* sig_out, double c0,
                                                  double c1, double c2, uint32_t n) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -413,8 +419,9 @@ __global__ void __launch_bounds__(256) k_streams(const double* __restrict__ x0,
     const double vx = v0[i], vy = v1[i], vz = v2[i];
     const uint32_t t = tag[i];
     const uint32_t sig = make_signature(t, vx, vy, vz);
+    const uint32_t tw = sp ? (t | ((uint32_t)sp[i] << 28)) : t;
     pos4[i] = make_float4((float)(x0[i] - c0), (float)(x1[i] - c1), (float)(x2[i] - c2),
-                          __uint_as_float(t));
+                          __uint_as_float(tw));
     vel4[i] = make_float4((float)vx, (float)vy, (float)vz, __uint_as_float(sig));
     if (sig_out) sig_out[i] = sig;
 }
@@ -695,13 +702,14 @@ struct BondArgs {
     float L[3], H[3];
     int periodic[3];
     uint32_t n, max_tag;
+    uint32_t tag_mask;  // 0x0FFFFFFF when species ride in pos4.w
 };
 
 __global__ void k_bonds(BondArgs a) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.n) return;
     const float4 pi = a.pos4[i];
-    const uint32_t tag = __float_as_uint(pi.w);
+    const uint32_t tag = __float_as_uint(pi.w) & a.tag_mask;
     if (tag > a.max_tag) return;
     const uint32_t b0 = a.boff[tag], b1 = a.boff[tag + 1];
     if (b0 == b1) return;

@@ -44,10 +44,33 @@ def oracle_forces(e, s, obox, params, step, seed=1, paper=False):
                          [obox.hi[k] - ctr[k] for k in range(3)],
                          tuple(obox.periodic))
     mix = O.lib().orc_step_mix(seed, step)
+    sp = np.ascontiguousarray(s.species, np.uint8) if params.n_species > 1 else None
     f = O.compute_forces(_sys.oparams(params), box, *x, *v, s.tag, sig, mix, t.entries,
                          t.core_count, t.skin_count, t.max_neighbors, tiled=t.tiled,
-                         joined=t.joined, nthreads=8)
+                         joined=t.joined, species=sp, nthreads=8)
     return np.stack(f, 1)
+
+
+def test_forces_multispecies_vesicle_matrix():
+    """Three species with the paper's repulsion matrix:
+    a(A,A)=a(A,S)=a(S,S)=a(B,B)=15, a(A,B)=a(B,S)=120, gamma 4.5 (sigma 3)."""
+    box, obox, st = _sys.fluid((10, 10, 10), 5.0, seed=31)
+    n = len(st[0])
+    species = np.random.default_rng(1).integers(0, 3, n).astype(np.uint8)  # A=0 B=1 S=2
+    a = np.array([[15, 120, 15], [120, 15, 120], [15, 120, 15]], np.float64).reshape(-1)
+    p = dpd.PairParams.make(3, a, 4.5, 1.0, 1.0, 1.0, 0.01)
+    e = dpd.Engine(box, p, dpd.RunConfig(), capacity=n)
+    e.upload(dpd.ParticleStore.from_arrays(*st, species=species))
+    e.reorder_particles()
+    e.build_neighbor_table()
+    Fg = np.stack(e.compute_forces(4), 1)
+    s = e.download()
+    F = oracle_forces(e, s, obox, p, 4)
+    assert np.linalg.norm(Fg - F) / np.linalg.norm(F) <= REL_L2
+    assert np.abs(Fg.sum(0)).max() <= 1e-3
+    e.setup()
+    e.step(50)
+    assert np.isfinite(e.thermo()["kbt"])
 
 
 @pytest.mark.parametrize("L,per,step", [((32, 32, 32), (1, 1, 1), 0),
