@@ -186,6 +186,56 @@ int dpdb_eval(int device, int op, size_t n, const void* in0, const void* in1, ui
  * arrays in/out, bit_length multiple of 4 and <= 32 */
 int dpdb_radix_sort(int device, uint32_t* keys, uint32_t* vals, size_t n, int bit_length);
 
+/* ------------------------------------------- brick decomposition (§8e)
+ * decompose / border_determination / exchange_ghosts / migrate_strays and
+ * the GhostPacket wire records of the spec (paper Alg. 6,
+ * P:316-331).  One context owns one brick: uniform half-open slabs of the
+ * global box, locals at [0, n), ghosts at [n, n + ng).  Directions
+ * d = 0..25 enumerate the neighbor offsets (dx, dy, dz) in z-major order
+ * with the centre removed; the opposite of d is 25 - d.  Every exchange
+ * buffer is DEVICE memory holding records in direction order; the transport
+ * (in-process peer copies below, or NCCL between processes) delivers to
+ * brick b, for each d, what the brick at b + d packed for direction 25 - d. */
+#define DPDB_MD_MIGRANTS 0     /* full record: x, v (f64), tag, species | molecule << 8 */
+#define DPDB_MD_GHOST_FULL 1   /* same record, x shifted by the periodic image */
+#define DPDB_MD_GHOST_UPDATE 2 /* x (shifted), v only; receiver order fixed at rebuild */
+
+/* decompose: the brick at `coords` of a dims[0]xdims[1]xdims[2] grid */
+int dpdb_create_domain(int device, const dpdb_box* box, const dpdb_params* params,
+                       const dpdb_run* run, const int32_t dims[3], const int32_t coords[3],
+                       size_t capacity, dpdb_ctx** out);
+int dpdb_domain_info(const dpdb_ctx* ctx, double slab_lo[3], double slab_hi[3], int32_t dims[3],
+                     int32_t coords[3]);
+/* coordinates of the neighbor brick in direction d; DPDB_ECONFIG if none */
+int dpdb_md_neighbor(const dpdb_ctx* ctx, int dir, int32_t nb_coords[3]);
+int dpdb_md_record_bytes(int what);
+/* Per-brick protocol.  Setup: begin_setup, accept_migrants(NULL, NULL, gc),
+ * exchange GHOST_FULL (gc), accept_ghosts, forces.  Rebuild step:
+ * begin_rebuild(mc), exchange MIGRANTS (mc), accept_migrants(.., gc),
+ * exchange GHOST_FULL (gc), accept_ghosts, forces.  Other steps: begin_step,
+ * exchange GHOST_UPDATE (the counts of the last rebuild), accept_update,
+ * forces.  finish applies the pending half-kick (end of the last step). */
+int dpdb_md_begin_setup(dpdb_ctx* ctx);
+int dpdb_md_begin_rebuild(dpdb_ctx* ctx, int32_t migrant_counts[26]);
+int dpdb_md_pack(dpdb_ctx* ctx, int what, void* dev_out);
+int dpdb_md_accept_migrants(dpdb_ctx* ctx, const void* dev_in, const int32_t counts[26],
+                            int32_t ghost_counts[26]);
+int dpdb_md_accept_ghosts(dpdb_ctx* ctx, const void* dev_in, const int32_t counts[26]);
+int dpdb_md_begin_step(dpdb_ctx* ctx);
+int dpdb_md_accept_update(dpdb_ctx* ctx, const void* dev_in, const int32_t counts[26]);
+int dpdb_md_forces(dpdb_ctx* ctx);
+int dpdb_md_finish(dpdb_ctx* ctx);
+/* sum of v, v^2 over the locals (for a cross-brick temperature) */
+int dpdb_md_sums(dpdb_ctx* ctx, double out[4]);
+int dpdb_md_ghost_count(const dpdb_ctx* ctx, size_t* ng);
+/* the ghosts [n, n + ng) as this brick holds them (x shifted to its image) */
+int dpdb_md_download_ghosts(dpdb_ctx* ctx, double* x, double* y, double* z, double* vx,
+                            double* vy, double* vz, uint32_t* tag);
+/* In-process transport: all bricks of a decomposition in one process (one
+ * or several GPUs; cudaMemcpyPeerAsync over NVLink between GPUs). */
+int dpdb_group_setup(dpdb_ctx* const* ctxs, int n_bricks);
+int dpdb_group_step(dpdb_ctx* const* ctxs, int n_bricks, int64_t nsteps);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,7 +96,29 @@ SYMBOLS = {
     "dpdb_eval": (C.c_int, [C.c_int, C.c_int, C.c_size_t, C.c_void_p, C.c_void_p, C.c_uint32,
                             C.c_void_p]),
     "dpdb_radix_sort": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int]),
+    # brick decomposition
+    "dpdb_create_domain": (C.c_int, [C.c_int, C.POINTER(Box), C.POINTER(Params), C.POINTER(Run),
+                                     C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]),
+    "dpdb_domain_info": (C.c_int, [C.c_void_p] + [C.c_void_p] * 4),
+    "dpdb_md_neighbor": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    "dpdb_md_record_bytes": (C.c_int, [C.c_int]),
+    "dpdb_md_begin_setup": (C.c_int, [C.c_void_p]),
+    "dpdb_md_begin_rebuild": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "dpdb_md_pack": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    "dpdb_md_accept_migrants": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "dpdb_md_accept_ghosts": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "dpdb_md_begin_step": (C.c_int, [C.c_void_p]),
+    "dpdb_md_accept_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "dpdb_md_forces": (C.c_int, [C.c_void_p]),
+    "dpdb_md_finish": (C.c_int, [C.c_void_p]),
+    "dpdb_md_sums": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "dpdb_md_ghost_count": (C.c_int, [C.c_void_p, C.POINTER(C.c_size_t)]),
+    "dpdb_md_download_ghosts": (C.c_int, [C.c_void_p] + [C.c_void_p] * 7),
+    "dpdb_group_setup": (C.c_int, [C.c_void_p, C.c_int]),
+    "dpdb_group_step": (C.c_int, [C.c_void_p, C.c_int, C.c_int64]),
 }
+
+MD_MIGRANTS, MD_GHOST_FULL, MD_GHOST_UPDATE = 0, 1, 2
 
 _lib = None
 

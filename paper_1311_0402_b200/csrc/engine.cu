@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <array>
 #include <vector>
 
 #include "dpdb.h"
@@ -22,6 +23,9 @@ using dpdb::HostGrid;
 
 namespace {
 thread_local std::string g_thread_err;
+// dpdb_create_domain passes the brick through these (same thread, same call)
+thread_local const int32_t* g_pending_dims = nullptr;
+thread_local const int32_t* g_pending_coords = nullptr;
 
 constexpr int BUILD_WARPS = 4;
 constexpr int BUILD_TILES = 2;
@@ -71,9 +75,22 @@ struct dpdb_ctx {
     std::vector<int> ev_stage;
     size_t ev_used = 0;
     int64_t launches[ST_N]{};
+    // brick decomposition (domain_host.inc); single domain: dims = 1
+    int dims[3]{1, 1, 1}, coords[3]{};
+    uint32_t md_valid = 0;     // bit d: a neighbor brick exists in direction d
+    double md_shift[26][3]{};  // periodic image shift of ghosts sent in direction d
+    size_t ng = 0;             // ghosts at [n, n + ng)
+    uint32_t *md_masks{}, *md_mig{}, *md_mlist{}, *md_glist{}, *md_slot{}, *md_doff{}, *md_dbase{};
+    size_t md_list_cap = 0;
+    uint32_t md_moff[27]{}, md_goff[27]{};
+    uint32_t md_n_out = 0, md_n_all = 0;
+    bool md_in_rebuild = false, md_pending_p2 = false;
+    std::array<int32_t, 26> md_gcnt{};
 };
 
 namespace {
+
+int md_dirs(const dpdb_ctx* ctx, int d, int nb[3]);  // domain_host.inc
 
 int fail(dpdb_ctx* ctx, int code, const std::string& msg) {
     if (ctx)
@@ -194,8 +211,12 @@ void wrap_lengths(const dpdb_ctx* ctx, float L[3], float H[3]) {
     }
 }
 
+// defer_wrap (brick runs, non-rebuild steps): no periodic wrap on axes split
+// across bricks -- a local that crosses the seam keeps its unwrapped
+// coordinate (consistent with its neighbors and with the shifted ghost
+// copies) until the next rebuild wraps and migrates it
 template <bool P2, bool P1, bool KEYS, bool STREAMS>
-int launch_integrate(dpdb_ctx* ctx) {
+int launch_integrate(dpdb_ctx* ctx, bool defer_wrap = false) {
     if (!ctx->n) return 0;
     dpdb::IntegrateArgs a{};
     for (int k = 0; k < 3; ++k) {
@@ -211,6 +232,9 @@ int launch_integrate(dpdb_ctx* ctx) {
     a.vals = ctx->vals;
     a.err = ctx->err;
     a.bnd = boundary(ctx);
+    if (defer_wrap)
+        for (int k = 0; k < 3; ++k)
+            if (ctx->dims[k] > 1) a.bnd.periodic[k] = 0;  // walls still reflect
     a.grid = dev_grid(ctx);
     a.dt = ctx->params.dt;
     a.h = 0.5 * ctx->params.dt;
@@ -534,9 +558,28 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
     ctx->multi = params->n_species > 1;
     for (int q = 0; q < ns * ns; ++q) ctx->sigma[q] = std::sqrt(2.0 * params->gamma[q] * params->kbt);
     std::string err;
-    const int dims[3] = {1, 1, 1}, crd[3] = {0, 0, 0};
-    int rc = ctx->grid.make(*box, box->lo, box->hi, dims, crd, params->r_c + run->skin,
+    // brick geometry (decompose): uniform half-open slabs
+    double slo[3], shi[3];
+    for (int k = 0; k < 3; ++k) {
+        ctx->dims[k] = g_pending_dims ? g_pending_dims[k] : 1;
+        ctx->coords[k] = g_pending_coords ? g_pending_coords[k] : 0;
+        const double len = (box->hi[k] - box->lo[k]) / ctx->dims[k];
+        slo[k] = box->lo[k] + ctx->coords[k] * len;
+        shi[k] = ctx->coords[k] == ctx->dims[k] - 1 ? box->hi[k] : box->lo[k] + (ctx->coords[k] + 1) * len;
+    }
+    int rc = ctx->grid.make(*box, slo, shi, ctx->dims, ctx->coords, params->r_c + run->skin,
                             run->sub_bits, err);
+    for (int d = 0; d < 26; ++d) {
+        int nb[3], off[3];
+        if (!md_dirs(ctx, d, nb)) continue;
+        ctx->md_valid |= 1u << d;
+        dpdb::dir_offset(d, off);
+        for (int k = 0; k < 3; ++k) {
+            const int c = ctx->coords[k] + off[k];
+            const double L = box->hi[k] - box->lo[k];
+            ctx->md_shift[d][k] = c >= ctx->dims[k] ? -L : (c < 0 ? L : 0.0);
+        }
+    }
     if (rc) {
         fail(nullptr, rc, err);
         delete ctx;
@@ -581,7 +624,8 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         (rc = dalloc(ctx, ctx->pos4, c)) || (rc = dalloc(ctx, ctx->vel4, c)) ||
         (rc = dalloc(ctx, ctx->keys, c)) || (rc = dalloc(ctx, ctx->keys2, c)) ||
         (rc = dalloc(ctx, ctx->vals, c)) || (rc = dalloc(ctx, ctx->vals2, c)) ||
-        (rc = dalloc(ctx, ctx->hist, (size_t)256 * tiles + 256)) ||
+        (rc = dalloc(ctx, ctx->hist, std::max<size_t>((size_t)256 * tiles + 256,
+                                                      26 * (c / dpdb::MD_THREADS + 1) + 64))) ||
         (rc = dalloc(ctx, ctx->cell_start, (size_t)g.n_total_cells + 1)) ||
         (rc = dalloc(ctx, ctx->rank_of_cell, (size_t)g.n_total_cells)) ||
         (rc = dalloc(ctx, ctx->stencil, (size_t)g.n_local_cells * 32)) ||
@@ -589,9 +633,15 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         (rc = dalloc(ctx, ctx->cell_flags, (size_t)g.n_local_cells)) ||
         (rc = dalloc(ctx, ctx->entries, c * ctx->maxn)) || (rc = dalloc(ctx, ctx->counts, c)) ||
         (rc = dalloc(ctx, ctx->fwalk, c)) || (rc = dalloc(ctx, ctx->rowmeta, c)) ||
+        (rc = dalloc(ctx, ctx->md_masks, c)) || (rc = dalloc(ctx, ctx->md_mig, c)) ||
+        (rc = dalloc(ctx, ctx->md_slot, c)) || (rc = dalloc(ctx, ctx->md_doff, 32)) ||
+        (rc = dalloc(ctx, ctx->md_dbase, 32)) ||
+        (rc = dalloc(ctx, ctx->md_mlist, ctx->md_valid ? 8 * c : 1)) ||
+        (rc = dalloc(ctx, ctx->md_glist, ctx->md_valid ? 8 * c : 1)) ||
         (rc = dalloc(ctx, ctx->err, 1)) || (rc = dalloc(ctx, ctx->red, (size_t)RED_BLOCKS * 4)) ||
         (rc = dalloc(ctx, ctx->red_out, 8)) || (rc = dalloc(ctx, ctx->tmp_u32, c)))
         return bail(rc);
+    ctx->md_list_cap = ctx->md_valid ? 8 * c : 1;  // a corner particle sits in 7 lists
     if (cudaMemset(ctx->err, 0, sizeof(DevErr)) != cudaSuccess ||
         cudaMemset(ctx->counts, 0, c * 4) != cudaSuccess ||
         cudaMemset(ctx->sp, 0, c) != cudaSuccess || cudaMemset(ctx->sp2, 0, c) != cudaSuccess ||
@@ -627,7 +677,8 @@ int dpdb_destroy(dpdb_ctx* ctx) {
                     ctx->cell_flags, ctx->entries, ctx->counts, ctx->fwalk, ctx->rowmeta,
                     ctx->err, ctx->red, ctx->red_out,
                     ctx->tmp_u32, ctx->bond_off, ctx->bond_partner, ctx->index_of_tag,
-                    ctx->bond_k, ctx->bond_r0};
+                    ctx->bond_k, ctx->bond_r0, ctx->md_masks, ctx->md_mig, ctx->md_slot,
+                    ctx->md_doff, ctx->md_dbase, ctx->md_mlist, ctx->md_glist};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (int k = 0; k < 3; ++k) {
@@ -1220,3 +1271,5 @@ int dpdb_radix_sort(int device, uint32_t* keys, uint32_t* vals, size_t n, int bi
 }
 
 }  // extern "C"
+
+#include "domain_host.inc"

@@ -685,6 +685,7 @@ __global__ void k_tile_transpose(uint32_t* entries, uint32_t n_rows_pad, uint32_
 }
 
 #include "force.cuh"
+#include "domain.cuh"
 
 // Harmonic bonds: F = -K (r - r0) e on each endpoint.  Bonds are
 // stored as a static CSR over TAGS (each bond at both endpoints), resolved

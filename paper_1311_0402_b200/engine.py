@@ -182,14 +182,23 @@ class Engine:
     neighbor table + forces) driven through the C ABI."""
 
     def __init__(self, box: SimBox, params: PairParams, run: RunConfig | None = None,
-                 capacity: int = 1, device: int = 0):
+                 capacity: int = 1, device: int = 0, dims=None, coords=None):
         self.box, self.params, self.run = box, params, run or RunConfig()
         self.device = device
         L = lib()
         h = C.c_void_p()
         self._cb, self._cp, self._cr = box._c(), params._c(), self.run._c()
-        check(L.dpdb_create(device, C.byref(self._cb), C.byref(self._cp), C.byref(self._cr),
-                            int(capacity), C.byref(h)))
+        if dims is None:
+            check(L.dpdb_create(device, C.byref(self._cb), C.byref(self._cp), C.byref(self._cr),
+                                int(capacity), C.byref(h)))
+        else:  # one brick of a decomposition (S:554-562)
+            d = np.ascontiguousarray(dims, np.int32)
+            c = np.ascontiguousarray(coords, np.int32)
+            check(L.dpdb_create_domain(device, C.byref(self._cb), C.byref(self._cp),
+                                       C.byref(self._cr), ptr(d), ptr(c), int(capacity),
+                                       C.byref(h)))
+        self.dims = tuple(int(v) for v in (dims if dims is not None else (1, 1, 1)))
+        self.coords = tuple(int(v) for v in (coords if coords is not None else (0, 0, 0)))
         self.h = h.value
         gi = GridInfo()
         check(L.dpdb_grid(self.h, C.byref(gi)), self.h)
