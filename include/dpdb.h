@@ -236,6 +236,23 @@ int dpdb_md_download_ghosts(dpdb_ctx* ctx, double* x, double* y, double* z, doub
 int dpdb_group_setup(dpdb_ctx* const* ctxs, int n_bricks);
 int dpdb_group_step(dpdb_ctx* const* ctxs, int n_bricks, int64_t nsteps);
 
+/* NCCL transport: one brick per process (rank = coords[0] + dims[0] *
+ * (coords[1] + dims[1] * coords[2])).  Rank 0 makes the id, the caller
+ * broadcasts it (e.g. over torch.distributed), every rank attaches.  The step
+ * then runs entirely on the brick's stream: pack -> grouped ncclSend/Recv per
+ * neighbor direction -> unpack -> forces, no host sync between rebuilds
+ * (a rebuild all-gathers 26 counts per rank).  NCCL is loaded at run time. */
+#define DPDB_NCCL_ID_BYTES 128
+int dpdb_nccl_unique_id(uint8_t id[DPDB_NCCL_ID_BYTES]);
+int dpdb_nccl_attach(dpdb_ctx* ctx, const uint8_t id[DPDB_NCCL_ID_BYTES], int nranks, int rank);
+int dpdb_dist_setup(dpdb_ctx* ctx);
+int dpdb_dist_step(dpdb_ctx* ctx, int64_t nsteps);
+/* device time of nsteps (ms, CUDA events on the brick's stream) and the
+ * number of engine kernels launched */
+int dpdb_dist_step_timed(dpdb_ctx* ctx, int64_t nsteps, double* ms, int64_t* launches);
+/* global thermo line: per-brick partial sums all-gathered, added in rank order */
+int dpdb_dist_thermo(dpdb_ctx* ctx, dpdb_thermo* out);
+
 #ifdef __cplusplus
 }
 #endif

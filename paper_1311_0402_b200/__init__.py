@@ -15,7 +15,7 @@ from .engine import (  # noqa: F401
     fastcos2pi, fastlog, fastpow, gaussian, make_signature, morton_encode, pair_uniforms,
     radix_sort, step_mix, tea_hash,
 )
-from .domain import BrickGroup, DistBrick, HaloExchange  # noqa: F401
+from .domain import BrickGroup, DistBrick, HaloExchange, NcclBrick  # noqa: F401
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 

@@ -85,12 +85,22 @@ struct dpdb_ctx {
     uint32_t md_moff[27]{}, md_goff[27]{};
     uint32_t md_n_out = 0, md_n_all = 0;
     bool md_in_rebuild = false, md_pending_p2 = false;
-    std::array<int32_t, 26> md_gcnt{};
+    std::array<int32_t, 26> md_gcnt{};  // ghosts this brick sends per direction
+    std::array<int32_t, 26> md_rcnt{};  // ghosts it receives per direction
+    void *md_sbuf{}, *md_rbuf{};         // packed records out / in (device)
+    size_t md_scap = 0, md_rcap = 0;
+    // NCCL transport (one brick per process)
+    void* nccl_comm = nullptr;
+    int nccl_rank = -1, nccl_size = 0;
+    int md_peer[26]{};
+    int32_t *md_dcnt{}, *md_hcnt{};      // device / pinned count exchange
+    double *md_dsum{}, *md_hsum{};       // device / pinned thermo exchange
 };
 
 namespace {
 
 int md_dirs(const dpdb_ctx* ctx, int d, int nb[3]);  // domain_host.inc
+void md_release(dpdb_ctx* ctx);                      // domain_host.inc
 
 int fail(dpdb_ctx* ctx, int code, const std::string& msg) {
     if (ctx)
@@ -634,7 +644,7 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         (rc = dalloc(ctx, ctx->entries, c * ctx->maxn)) || (rc = dalloc(ctx, ctx->counts, c)) ||
         (rc = dalloc(ctx, ctx->fwalk, c)) || (rc = dalloc(ctx, ctx->rowmeta, c)) ||
         (rc = dalloc(ctx, ctx->md_masks, c)) || (rc = dalloc(ctx, ctx->md_mig, c)) ||
-        (rc = dalloc(ctx, ctx->md_slot, c)) || (rc = dalloc(ctx, ctx->md_doff, 32)) ||
+        (rc = dalloc(ctx, ctx->md_slot, c)) || (rc = dalloc(ctx, ctx->md_doff, 64)) ||
         (rc = dalloc(ctx, ctx->md_dbase, 32)) ||
         (rc = dalloc(ctx, ctx->md_mlist, ctx->md_valid ? 8 * c : 1)) ||
         (rc = dalloc(ctx, ctx->md_glist, ctx->md_valid ? 8 * c : 1)) ||
@@ -671,6 +681,7 @@ int dpdb_destroy(dpdb_ctx* ctx) {
     if (!ctx) return 0;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    md_release(ctx);
     void* ptrs[] = {ctx->tag, ctx->tag2, ctx->mol, ctx->mol2, ctx->sp, ctx->sp2, ctx->pos4,
                     ctx->vel4, ctx->keys, ctx->keys2, ctx->vals, ctx->vals2, ctx->hist,
                     ctx->cell_start, ctx->rank_of_cell, ctx->stencil, ctx->stencil_n,

@@ -28,7 +28,8 @@ import ctypes as C
 
 import numpy as np
 
-from ._lib import MD_GHOST_FULL, MD_GHOST_UPDATE, MD_MIGRANTS, DPDError, check, lib, ptr
+from ._lib import (MD_GHOST_FULL, MD_GHOST_UPDATE, MD_MIGRANTS, NCCL_ID_BYTES, DPDError, Thermo,
+                   check, lib, ptr)
 from .engine import Engine, PairParams, ParticleStore, RunConfig, SimBox
 
 N_DIRS = 26
@@ -142,9 +143,9 @@ def gather_stores(parts):
 def thermo_from_sums(sums, n):
     """Global temperature/momentum from per-brick (sum v, sum |v|^2)."""
     s = np.sum(np.asarray(sums, np.float64).reshape(-1, 4), 0)
-    mom = s[:3] / n
-    kbt = (s[3] - n * float(mom @ mom)) / (3.0 * n)
-    return dict(n=int(n), kbt=float(kbt), momentum=tuple(float(v) for v in mom))
+    kbt = (s[3] - float(s[:3] @ s[:3]) / n) / (3.0 * n)
+    # momentum = total (unit masses), as Engine.thermo / dpdb_thermo_get
+    return dict(n=int(n), kbt=float(kbt), momentum=tuple(float(v) for v in s[:3]))
 
 
 class _Brick(Engine):
@@ -408,4 +409,74 @@ class DistBrick:
         part = self.brick.download()
         out = [None] * self.x.world
         self.x.dist.all_gather_object(out, part, group=self.group)
+        return gather_stores(out)
+
+
+class NcclBrick:
+    """One brick per rank on the engine's own NCCL transport: the whole step
+    loop (pack -> grouped ncclSend/Recv per direction -> unpack -> forces)
+    runs in libdpdb.so on the brick's stream.  torch.distributed (any
+    backend) only broadcasts the NCCL id and times the run."""
+
+    def __init__(self, box: SimBox, params: PairParams, run: RunConfig | None, dims, capacity,
+                 device=0, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.dims = tuple(int(v) for v in dims)
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        if self.world != self.dims[0] * self.dims[1] * self.dims[2]:
+            raise DPDError(1, "nccl brick: world size must equal the number of bricks")
+        self.coords = coords_of(self.rank, self.dims)
+        self.box, self.run = box, run or RunConfig()
+        self.brick = _Brick(box, params, self.run, capacity, device, self.dims, self.coords)
+        uid = np.zeros(NCCL_ID_BYTES, np.uint8)
+        if self.rank == 0:
+            check(lib().dpdb_nccl_unique_id(ptr(uid)))
+        obj = [uid.tobytes()]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        uid = np.frombuffer(obj[0], np.uint8).copy()
+        check(lib().dpdb_nccl_attach(self.brick.h, ptr(uid), self.world, self.rank), self.brick.h)
+
+    @property
+    def h(self):
+        return self.brick.h
+
+    def close(self):
+        self.brick.close()
+
+    def upload(self, part: ParticleStore):
+        """This brick's own particles (all inside its slab)."""
+        self.brick.upload(part)
+
+    def upload_global(self, store: ParticleStore):
+        self.brick.upload(split_store(store, self.box, self.dims)[self.rank])
+
+    def setup(self):
+        check(lib().dpdb_dist_setup(self.h), self.h)
+
+    def step(self, nsteps: int = 1):
+        check(lib().dpdb_dist_step(self.h, int(nsteps)), self.h)
+
+    def step_timed(self, nsteps: int):
+        ms, ln = C.c_double(), C.c_int64()
+        check(lib().dpdb_dist_step_timed(self.h, int(nsteps), C.byref(ms), C.byref(ln)), self.h)
+        return ms.value, ln.value
+
+    def thermo(self):
+        t = Thermo()
+        check(lib().dpdb_dist_thermo(self.h, C.byref(t)), self.h)
+        return dict(step=t.step, n=t.n, kbt=t.kbt, momentum=tuple(t.momentum))
+
+    @property
+    def current_step(self):
+        return self.brick.current_step
+
+    def download(self):
+        return self.brick.download()
+
+    def download_global(self):
+        part = self.brick.download()
+        out = [None] * self.world
+        self.dist.all_gather_object(out, part, group=self.group)
         return gather_stores(out)

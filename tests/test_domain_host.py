@@ -106,7 +106,7 @@ def test_thermo_from_sums():
     sums = [np.concatenate([p.sum(0), [(p * p).sum()]]) for p in parts]
     t = D.thermo_from_sums(sums, len(v))
     m = v.mean(0)
-    assert np.allclose(t["momentum"], m)
+    assert np.allclose(t["momentum"], v.sum(0))  # total momentum, unit masses
     assert abs(t["kbt"] - ((v - m) ** 2).sum() / (3 * len(v))) < 1e-12
 
 
