@@ -9,9 +9,13 @@ table 2.1 GB) are far larger than the 126 MB L2, so no explicit L2 flush.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-Under torchrun each rank simulates its own 4M box (replicas: the spatial
-brick decomposition is not built yet), timed on the device with CUDA events,
-max over ranks; rank 0 prints one JSON line.
+Under torchrun (N > 1) the box is decomposed into N bricks of 4M particles
+each (weak scaling: 2x1x1 / 2x2x1 / 2x2x2, periodic), one brick
+per GPU: halo update every step and migration + full halo every rebuild over
+the engine's own NCCL transport (grouped ncclSend/Recv per neighbor
+direction on the brick's stream).  Timed on the device with CUDA events, max
+over ranks; rank 0 prints one JSON line.  --mode replicas runs N independent
+4M boxes instead.
 """
 from __future__ import annotations
 
@@ -191,7 +195,7 @@ def run_reference(args, ws, rank):
         "impl": "reference", "metric": METRIC, "value": round(val, 4), "unit": UNIT,
         "n_gpus": args.gpus, "steps": nsteps, "warmup": 0, "ms_per_step": N_C3 / (val * 1e6) * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_dict(ws),
+        "data": "synthetic", "config": config_dict(ws, args.mode),
         "cpu_baseline": {"value": round(val, 4), "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": round(val, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -200,27 +204,93 @@ def run_reference(args, ws, rank):
     print(json.dumps(line), flush=True)
 
 
-def config_dict(ws):
+def brick_dims(ws):
+    """Most cubic factorisation of ws into 3 brick counts (x fastest)."""
+    best = None
+    for a in range(1, ws + 1):
+        for b in range(1, ws + 1):
+            if ws % (a * b):
+                continue
+            c = ws // (a * b)
+            d = tuple(sorted((a, b, c), reverse=True))
+            if best is None or max(d) - min(d) < max(best) - min(best):
+                best = d
+    return best
+
+
+def config_dict(ws, mode="bricks"):
+    par = "single"
+    if ws > 1:
+        par = (f"bricks{'x'.join(map(str, brick_dims(ws)))}" if mode == "bricks"
+               else f"replicas{ws}")
     return {"workload": "C3: homogeneous DPD fluid, 4,194,304 particles per GPU, rho=3, "
-                        "L=111.818, a=25, gamma=4.5, kT=1, rc=1, dt=0.01, skin=0.3, rebuild=10",
+                        "L=111.818 per GPU, a=25, gamma=4.5, kT=1, rc=1, dt=0.01, skin=0.3, "
+                        "rebuild=10",
             "particles_per_gpu": N_C3, "rho": RHO, "rebuild_every": 10, "max_neighbors": 128,
-            "parallelism": f"replicas{ws}" if ws > 1 else "single",
+            "parallelism": par,
             "l2": "inputs > L2 (0.7 GB state + 2.1 GB table vs 126 MB L2); no flush"}
 
 
 # --------------------------------------------------------------- B200 arm
+class _BrickRunner:
+    """Adapter giving a NcclBrick the Engine calls the bench makes."""
+
+    def __init__(self, nb):
+        self.nb = nb
+
+    def upload(self, store):
+        self.nb.upload(store)
+
+    def setup(self):
+        self.nb.setup()
+
+    def step(self, k):
+        self.nb.step(k)
+
+    def step_timed(self, k, stages=True):
+        return self.nb.step_timed(k, stages=stages)
+
+    def thermo(self):
+        return self.nb.thermo()
+
+    def download(self):
+        return self.nb.download()
+
+    def table_stats(self):
+        return self.nb.brick.table_stats()
+
+    def close(self):
+        self.nb.close()
+
+
 def run_b200(args, ws, rank, local):
     import torch
 
     import paper_1311_0402_b200 as dpd
+    from paper_1311_0402_b200 import domain as D
 
     torch.cuda.set_device(local)
     L = c3_box()
-    state = synth_state(N_C3, L, seed=2024 + rank)
-    box = dpd.SimBox((0.0, 0.0, 0.0), (L, L, L))
     params = dpd.PairParams()
     run = dpd.RunConfig()
-    e = dpd.Engine(box, params, run, capacity=N_C3, device=local)
+    bricks = ws > 1 and args.mode == "bricks"
+    if bricks:
+        # weak scaling: N bricks of the C3 cube, one per GPU, 4M particles each
+        dims = brick_dims(ws)
+        box = dpd.SimBox((0.0, 0.0, 0.0), tuple(L * d for d in dims))
+        coords = D.coords_of(rank, dims)
+        lo, hi = D.slab_bounds(box, dims, coords)
+        state = synth_state(N_C3, L, seed=2024 + rank)
+        for k in range(3):  # place this rank's particles inside its own slab
+            state[k] = np.minimum(lo[k] + state[k] * ((hi[k] - lo[k]) / L),
+                                  np.nextafter(hi[k], lo[k]))
+        state[6] = state[6] + np.uint32(rank * N_C3)
+        e = _BrickRunner(D.NcclBrick(box, params, run, dims, capacity=int(N_C3 * 1.2),
+                                     device=local))
+    else:
+        state = synth_state(N_C3, L, seed=2024 + rank)
+        box = dpd.SimBox((0.0, 0.0, 0.0), (L, L, L))
+        e = dpd.Engine(box, params, run, capacity=N_C3, device=local)
     e.upload(dpd.ParticleStore.from_arrays(*state))
     e.setup()
     e.step(args.warmup)
@@ -277,7 +347,7 @@ def run_b200(args, ws, rank, local):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 5),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (uniform positions, Maxwell-Boltzmann velocities, seed 2024+rank)",
-        "config": config_dict(ws),
+        "config": config_dict(ws, args.mode),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": traffic, "kernel": "k_force",
@@ -288,6 +358,8 @@ def run_b200(args, ws, rank, local):
                           "frac": round(step_bytes / (step_ms * 1e-3) / 1e9 / peak, 4)},
         "stage_ms_per_step": {k: round(stage_ms[i] / args.steps, 5) for i, k in
                               enumerate(["integrate", "sort_permute", "build", "force", "other"])},
+        "stage_note": ("bricks: build = whole rebuild step (integrate, migration, full halo, "
+                       "sort, build); other = halo update") if bricks else None,
         "gpu_launches": int(launches[5]),
         "e2e": {"value": round(e2e, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d / args.steps),
                 "d2h_bytes_per_step": int(d2h),
@@ -312,6 +384,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", default=25.0, type=float)
+    ap.add_argument("--mode", default="bricks", choices=["bricks", "replicas"],
+                    help="N > 1: brick decomposition over NCCL (default) or independent replicas")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

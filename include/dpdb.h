@@ -247,9 +247,11 @@ int dpdb_nccl_unique_id(uint8_t id[DPDB_NCCL_ID_BYTES]);
 int dpdb_nccl_attach(dpdb_ctx* ctx, const uint8_t id[DPDB_NCCL_ID_BYTES], int nranks, int rank);
 int dpdb_dist_setup(dpdb_ctx* ctx);
 int dpdb_dist_step(dpdb_ctx* ctx, int64_t nsteps);
-/* device time of nsteps (ms, CUDA events on the brick's stream) and the
- * number of engine kernels launched */
-int dpdb_dist_step_timed(dpdb_ctx* ctx, int64_t nsteps, double* ms, int64_t* launches);
+/* as dpdb_step_timed: device time (ms, CUDA events on the brick's stream),
+ * stage_ms[0..5] = integrate, (unused), rebuild (migration + full halo + sort
+ * + build), force, other (halo update), total; stage_launches likewise */
+int dpdb_dist_step_timed(dpdb_ctx* ctx, int64_t nsteps, double* ms, double* stage_ms,
+                         int64_t* stage_launches);
 /* global thermo line: per-brick partial sums all-gathered, added in rank order */
 int dpdb_dist_thermo(dpdb_ctx* ctx, dpdb_thermo* out);
 

@@ -120,8 +120,8 @@ SYMBOLS = {
     "dpdb_nccl_attach": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
     "dpdb_dist_setup": (C.c_int, [C.c_void_p]),
     "dpdb_dist_step": (C.c_int, [C.c_void_p, C.c_int64]),
-    "dpdb_dist_step_timed": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_double),
-                                       C.POINTER(C.c_int64)]),
+    "dpdb_dist_step_timed": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_double), C.c_void_p,
+                                       C.c_void_p]),
     "dpdb_dist_thermo": (C.c_int, [C.c_void_p, C.POINTER(Thermo)]),
 }
 

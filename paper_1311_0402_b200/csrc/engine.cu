@@ -507,6 +507,50 @@ int require_ctx(const dpdb_ctx* ctx) {
     return 0;
 }
 
+// Runs body() between two events on the context stream; stage_ms[0..5]
+// from the mark() events body records (the time since the previous mark goes
+// to the stage the mark names), stage_launches from the launch counters.
+template <class F>
+int timed_run(dpdb_ctx* ctx, F&& body, double* ms, double* stage_ms, int64_t* stage_launches) {
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    for (int s = 0; s < ST_N; ++s) ctx->launches[s] = 0;
+    ctx->timing = stage_ms != nullptr;
+    ctx->ev_used = 0;
+    CK(cudaEventRecord(e0, ctx->stream));
+    const int rc = body();
+    cudaEventRecord(e1, ctx->stream);
+    ctx->timing = false;
+    if (rc) return rc;
+    TRY(check_device(ctx));
+    float total = 0;
+    CK(cudaEventElapsedTime(&total, e0, e1));
+    if (ms) *ms = total;
+    if (stage_ms) {
+        for (int s = 0; s <= ST_N; ++s) stage_ms[s] = 0;
+        cudaEvent_t prev = e0;
+        for (size_t q = 0; q < ctx->ev_used; ++q) {
+            float d = 0;
+            cudaEventElapsedTime(&d, prev, ctx->ev_pool[q]);
+            stage_ms[ctx->ev_stage[q]] += d;
+            prev = ctx->ev_pool[q];
+        }
+        stage_ms[ST_N] = total;
+    }
+    if (stage_launches) {
+        int64_t tot = 0;
+        for (int s = 0; s < ST_N; ++s) {
+            stage_launches[s] = ctx->launches[s];
+            tot += ctx->launches[s];
+        }
+        stage_launches[ST_N] = tot;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return 0;
+}
+
 }  // namespace
 
 // ====================================================================== ABI
@@ -1120,6 +1164,7 @@ int run_steps(dpdb_ctx* ctx, int64_t nsteps) {
     }
     return 0;
 }
+
 }  // namespace
 
 int dpdb_step(dpdb_ctx* ctx, int64_t nsteps) {
@@ -1133,43 +1178,7 @@ int dpdb_step_timed(dpdb_ctx* ctx, int64_t nsteps, double* ms, double* stage_ms,
                     int64_t* stage_launches) {
     TRY(require_ctx(ctx));
     CK(cudaSetDevice(ctx->device));
-    cudaEvent_t e0, e1;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
-    for (int s = 0; s < ST_N; ++s) ctx->launches[s] = 0;
-    ctx->timing = stage_ms != nullptr;
-    ctx->ev_used = 0;
-    CK(cudaEventRecord(e0, ctx->stream));
-    int rc = run_steps(ctx, nsteps);
-    cudaEventRecord(e1, ctx->stream);
-    ctx->timing = false;
-    if (rc) return rc;
-    TRY(check_device(ctx));
-    float total = 0;
-    CK(cudaEventElapsedTime(&total, e0, e1));
-    if (ms) *ms = total;
-    if (stage_ms) {
-        for (int s = 0; s <= ST_N; ++s) stage_ms[s] = 0;
-        cudaEvent_t prev = e0;
-        for (size_t q = 0; q < ctx->ev_used; ++q) {
-            float d = 0;
-            cudaEventElapsedTime(&d, prev, ctx->ev_pool[q]);
-            stage_ms[ctx->ev_stage[q]] += d;
-            prev = ctx->ev_pool[q];
-        }
-        stage_ms[ST_N] = total;
-    }
-    if (stage_launches) {
-        int64_t tot = 0;
-        for (int s = 0; s < ST_N; ++s) {
-            stage_launches[s] = ctx->launches[s];
-            tot += ctx->launches[s];
-        }
-        stage_launches[ST_N] = tot;
-    }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    return 0;
+    return timed_run(ctx, [&] { return run_steps(ctx, nsteps); }, ms, stage_ms, stage_launches);
 }
 
 int64_t dpdb_current_step(const dpdb_ctx* ctx) { return ctx ? ctx->step : -1; }

@@ -458,10 +458,14 @@ class NcclBrick:
     def step(self, nsteps: int = 1):
         check(lib().dpdb_dist_step(self.h, int(nsteps)), self.h)
 
-    def step_timed(self, nsteps: int):
-        ms, ln = C.c_double(), C.c_int64()
-        check(lib().dpdb_dist_step_timed(self.h, int(nsteps), C.byref(ms), C.byref(ln)), self.h)
-        return ms.value, ln.value
+    def step_timed(self, nsteps: int, stages: bool = False):
+        """(ms, stage_ms[6] or None, stage_launches[6]) like Engine.step_timed."""
+        ms = C.c_double()
+        st = np.zeros(6) if stages else None
+        ln = np.zeros(6, np.int64)
+        check(lib().dpdb_dist_step_timed(self.h, int(nsteps), C.byref(ms), ptr(st), ptr(ln)),
+              self.h)
+        return ms.value, st, ln
 
     def thermo(self):
         t = Thermo()

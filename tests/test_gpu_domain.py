@@ -274,7 +274,9 @@ def _nccl_worker(rank, world, port, dims, steps, out):
         b.upload_global(dpd.ParticleStore.from_arrays(*st))
         b.setup()
         b.step(steps)
-        ms, launches = b.step_timed(3)
+        ms, stage_ms, launches = b.step_timed(3, stages=True)
+        launches = int(launches[5])
+        assert abs(stage_ms[5] - ms) < 1e-6 and stage_ms[3] > 0
         s = b.download_global()
         t = b.thermo()
         if rank == 0:
