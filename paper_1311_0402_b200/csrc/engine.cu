@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <array>
@@ -55,7 +56,8 @@ struct dpdb_ctx {
     uint8_t *stencil_n{}, *cell_flags{};
     uint32_t *entries{}, *counts{}, *fwalk{};
     uint2* rowmeta{};
-    bool walk = false;  // table in the builder's force-walk layout (see k_build)
+    int walk = 0;         // table layout: 0 reference (split/joined), 1 ballot walk (k_build), 2 lane walk (k_build_lane)
+    bool lane_builder = true;  // k_build_lane (default) or the ballot k_build (DPDB_BUILDER=ballot)
     DevErr* err{};
     double *red{}, *red_out{};
     uint32_t* tmp_u32{};
@@ -363,7 +365,7 @@ int do_build(dpdb_ctx* ctx, bool joined_out) {
     if (!ctx->have_sorted) return fail(ctx, DPDB_ECONFIG, "build_neighbor_table: particles not reordered");
     ctx->tiled = true;
     ctx->joined = joined_out;
-    ctx->walk = joined_out;
+    ctx->walk = joined_out ? (ctx->lane_builder ? 2 : 1) : 0;
     ctx->have_table = true;
     if (!ctx->n) return 0;
     dpdb::BuildArgs a{};
@@ -387,6 +389,15 @@ int do_build(dpdb_ctx* ctx, bool joined_out) {
     a.cut_c = (float)(rc * rc);
     a.cut_s = (float)(rs * rs);
     wrap_lengths(ctx, a.L, a.H);
+    if (ctx->lane_builder) {
+        if (joined_out)
+            dpdb::k_build_lane<true><<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(a);
+        else
+            dpdb::k_build_lane<false><<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(a);
+        CKL();
+        ctx->launches[ST_BUILD]++;
+        return 0;
+    }
     constexpr int P = 32 * BUILD_TILES;
     const size_t smem = build_smem(ctx);
     if (joined_out)
@@ -609,6 +620,7 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
     ctx->params = *params;
     ctx->run = *run;
     ctx->maxn = run->max_neighbors;
+    if (const char* b = std::getenv("DPDB_BUILDER")) ctx->lane_builder = std::strcmp(b, "ballot") != 0;
     ctx->multi = params->n_species > 1;
     for (int q = 0; q < ns * ns; ++q) ctx->sigma[q] = std::sqrt(2.0 * params->gamma[q] * params->kbt);
     std::string err;
@@ -996,34 +1008,53 @@ int dpdb_build_neighbors(dpdb_ctx* ctx) {
 }
 
 namespace {
-// Restore the reference's joined rows (core ascending, skin ascending) from the
-// builder's force-walk layout using rowmeta (c1, c2, s1, s2; see k_build):
-// walk order = core[0,c1) core[c2,nc) skin[0,s1) skin[s2,ns) core[c1,c2) skin[s1,s2).
+// Restore the reference's joined rows (core ascending, skin ascending) from a
+// force-walk layout:
+//  1 (k_build): rowmeta (c1, c2, s1, s2), walk order = core[0,c1) core[c2,nc)
+//    skin[0,s1) skin[s2,ns) core[c1,c2) skin[s1,s2);
+//  2 (k_build_lane): n_front = fwalk & 0x1FFF entries ascending from the front,
+//    the rest reversed from the back; bit 31 marks skin entries.
 int unwalk(dpdb_ctx* ctx) {
     if (!ctx->walk) return 0;
+    const int layout = ctx->walk;
     const size_t n = ctx->n, rows = (n + 31) & ~(size_t)31, maxn = ctx->maxn;
-    ctx->walk = false;
+    ctx->walk = 0;
     if (!rows) return 0;
-    std::vector<uint32_t> raw(rows * maxn), cnt(n), out(rows * maxn, 0u);
+    std::vector<uint32_t> raw(rows * maxn), cnt(n), fw(n), out(rows * maxn, 0u);
     std::vector<uint2> meta(n);
     CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaMemcpy(raw.data(), ctx->entries, raw.size() * 4, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(cnt.data(), ctx->counts, n * 4, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(meta.data(), ctx->rowmeta, n * sizeof(uint2), cudaMemcpyDeviceToHost));
+    if (layout == 1) CK(cudaMemcpy(meta.data(), ctx->rowmeta, n * sizeof(uint2), cudaMemcpyDeviceToHost));
+    if (layout == 2) CK(cudaMemcpy(fw.data(), ctx->fwalk, n * 4, cudaMemcpyDeviceToHost));
     auto idx = [&](size_t i, size_t k) { return ((i & ~size_t(31)) + (k & 31)) * maxn + (k & ~size_t(31)) + (i & 31); };
-    std::vector<uint32_t> row(maxn);
+    std::vector<uint32_t> row(maxn), core, skin;
     for (size_t i = 0; i < n; ++i) {
         const uint32_t nc = cnt[i] & 0x1FFFu, ns = (cnt[i] >> 13) & 0x1FFFu;
-        const uint32_t c1 = meta[i].x & 0xFFFFu, c2 = meta[i].x >> 16;
-        const uint32_t s1 = meta[i].y & 0xFFFFu, s2 = meta[i].y >> 16;
-        const uint32_t A = c1, B = A + (nc - c2), C = B + s1, D = C + (ns - s2), E = D + (c2 - c1);
         uint32_t w = 0;
-        for (uint32_t k = 0; k < A; ++k) row[w++] = raw[idx(i, k)];
-        for (uint32_t k = D; k < E; ++k) row[w++] = raw[idx(i, k)];
-        for (uint32_t k = A; k < B; ++k) row[w++] = raw[idx(i, k)];
-        for (uint32_t k = B; k < C; ++k) row[w++] = raw[idx(i, k)];
-        for (uint32_t k = E; k < nc + ns; ++k) row[w++] = raw[idx(i, k)];
-        for (uint32_t k = C; k < D; ++k) row[w++] = raw[idx(i, k)];
+        if (layout == 1) {
+            const uint32_t c1 = meta[i].x & 0xFFFFu, c2 = meta[i].x >> 16;
+            const uint32_t s1 = meta[i].y & 0xFFFFu, s2 = meta[i].y >> 16;
+            const uint32_t A = c1, B = A + (nc - c2), C = B + s1, D = C + (ns - s2), E = D + (c2 - c1);
+            for (uint32_t k = 0; k < A; ++k) row[w++] = raw[idx(i, k)];
+            for (uint32_t k = D; k < E; ++k) row[w++] = raw[idx(i, k)];
+            for (uint32_t k = A; k < B; ++k) row[w++] = raw[idx(i, k)];
+            for (uint32_t k = B; k < C; ++k) row[w++] = raw[idx(i, k)];
+            for (uint32_t k = E; k < nc + ns; ++k) row[w++] = raw[idx(i, k)];
+            for (uint32_t k = C; k < D; ++k) row[w++] = raw[idx(i, k)];
+        } else {
+            const uint32_t tot = std::min<uint32_t>(nc + ns, (uint32_t)maxn);
+            const uint32_t nf = std::min<uint32_t>(fw[i] & 0x1FFFu, tot), nb = tot - nf;
+            core.clear();
+            skin.clear();
+            auto put = [&](uint32_t e) { (e >> 31 ? skin : core).push_back(e & 0x7FFFFFFFu); };
+            for (uint32_t k = 0; k < nf; ++k) put(raw[idx(i, k)]);
+            for (uint32_t q = 0; q < nb; ++q) put(raw[idx(i, maxn - 1 - q)]);
+            std::sort(core.begin(), core.end());
+            std::sort(skin.begin(), skin.end());
+            for (uint32_t e : core) row[w++] = e;
+            for (uint32_t e : skin) row[w++] = e;
+        }
         for (uint32_t k = 0; k < w; ++k) out[idx(i, k)] = row[k];
     }
     CK(cudaMemcpy(ctx->entries, out.data(), out.size() * 4, cudaMemcpyHostToDevice));

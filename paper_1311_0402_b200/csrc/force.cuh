@@ -116,9 +116,10 @@ __device__ __forceinline__ uint32_t row_offset(uint32_t lane, uint32_t m, uint32
 // to run, and Newton's third law holds exactly.  Row entries and candidate
 // positions are software-pipelined (entries 3 ahead, positions 1 ahead).
 //
-// WALK: the table is in the builder's walk layout (k_build<..., true>): each
-// row lists first the entries this particle evaluates and n_eval = fwalk & 0x1FFF,
-// so the in-block j < i entries are never loaded.
+// WALK: the table is in the builder's walk layout (k_build_lane<true>): each
+// row lists first the entries this particle evaluates (n_eval = fwalk & 0x1FFF,
+// skin entries tagged with bit 31), so the in-block j < i entries are never
+// loaded.
 //
 // GENERAL: any weight exponent s and n_species > 1 (pos4.w = tag |
 // species << 28, C/D/R coefficients from the ns x ns tables of PairParams,
@@ -219,9 +220,10 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(ForceArgs a) {
         const uint32_t* erow = a.entries + (size_t)(b0 + il0) * maxn + lane;
         uint32_t e0 = 0, e1 = 0, e2 = 0;
         constexpr bool JN = JOINED || WALK;
-        if (0 < tot) e0 = __ldg(erow + row_offset<TILED, JN>(lane, 0, nc, maxn));
-        if (1 < tot) e1 = __ldg(erow + row_offset<TILED, JN>(lane, 1, nc, maxn));
-        if (2 < tot) e2 = __ldg(erow + row_offset<TILED, JN>(lane, 2, nc, maxn));
+        constexpr uint32_t EMASK = WALK ? 0x7FFFFFFFu : 0xFFFFFFFFu;  // walk: bit 31 = skin
+        if (0 < tot) e0 = __ldg(erow + row_offset<TILED, JN>(lane, 0, nc, maxn)) & EMASK;
+        if (1 < tot) e1 = __ldg(erow + row_offset<TILED, JN>(lane, 1, nc, maxn)) & EMASK;
+        if (2 < tot) e2 = __ldg(erow + row_offset<TILED, JN>(lane, 2, nc, maxn)) & EMASK;
         float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f);
         if (0 < tot) p0 = __ldg(a.pos4 + e0);
         for (uint32_t m = 0; m < maxtot; ++m) {
@@ -232,7 +234,7 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(ForceArgs a) {
             const bool act = m < tot && (WALK || !(inblk && jl < il));  // lower index takes it
             e0 = e1;
             e1 = e2;
-            if (m + 3 < tot) e2 = __ldg(erow + row_offset<TILED, JN>(lane, m + 3, nc, maxn));
+            if (m + 3 < tot) e2 = __ldg(erow + row_offset<TILED, JN>(lane, m + 3, nc, maxn)) & EMASK;
             if (m + 1 < tot) p0 = __ldg(a.pos4 + e0);
             float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
             if (fl) {

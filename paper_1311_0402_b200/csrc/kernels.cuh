@@ -650,6 +650,104 @@ __global__ void __launch_bounds__(WARPS * 32) k_build(BuildArgs a) {
     }
 }
 
+// Lane-per-row ordered builder (same rows as k_build, bit for bit).  Lane l
+// of a warp owns row i = 32w + l and walks its own 27 stencil cells in
+// ascending rank order and each cell's particles in ascending index order, so
+// its row comes out strictly ascending with no atomics, no sort and no
+// cross-lane staging; the next stencil cell's range is prefetched one cell
+// ahead.  Consecutive rows share most stencil cells (Morton order), so the
+// candidate loads of a warp mostly hit the same L1 lines.  Entries are stored
+// straight into the 32x32 tile-transposed layout (raw_index):
+//   !WALK: the reference split layout, core from the front, skin reversed
+//          from the back (inc/neighbor_table.hpp:18-40);
+//    WALK: the force walk -- the entries the force kernel evaluates (j outside
+//          i's force block, or j > i) ascending from the front, skin entries
+//          tagged with bit 31; the in-block j < i entries (that pair is taken
+//          by j) from the back.  fwalk = n_front | force flags << 26.
+template <bool WALK>
+__global__ void __launch_bounds__(256) k_build_lane(BuildArgs a) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool row = i < a.n_local;
+    if (__all_sync(0xFFFFFFFFu, !row)) return;
+    const uint32_t maxn = a.maxn;
+    const uint32_t rl = a.n_local_cells - 1u;  // clamp: a bad key already raised an error
+    uint32_t r = 0, ns = 0, fl = 0;
+    float4 pi = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (row) {
+        r = min(a.keys[i] >> a.key_shift, rl);
+        ns = a.stencil_n[r];
+        fl = a.cell_flags[r];
+        pi = a.pos4[i];
+    }
+    const uint32_t wfl = fl & 7u;
+    const bool anywrap = __any_sync(0xFFFFFFFFu, wfl != 0u);
+    const uint32_t* srow = a.stencil + (size_t)r * 32;
+    const uint32_t fb0 = i & ~(a.force_block - 1u);
+    uint32_t s = 0, j = 0, jend = 0, nx_s = 0, nx_e = 0;
+    if (ns > 0) {
+        const uint32_t sc = srow[0];
+        j = a.cell_start[sc];
+        jend = a.cell_start[sc + 1];
+    }
+    if (ns > 1) {
+        const uint32_t sc = srow[1];
+        nx_s = a.cell_start[sc];
+        nx_e = a.cell_start[sc + 1];
+    }
+    uint32_t* rowp = a.entries + (size_t)(i & ~31u) * maxn + (i & 31u);
+    uint32_t kf = 0, kb = 0, nc = 0, nsk = 0;
+    bool active = ns > 0;
+    while (true) {
+        while (active && j >= jend) {  // next non-empty stencil cell
+            if (++s >= ns) {
+                active = false;
+                break;
+            }
+            j = nx_s;
+            jend = nx_e;
+            if (s + 1 < ns) {
+                const uint32_t sc = srow[s + 1];
+                nx_s = a.cell_start[sc];
+                nx_e = a.cell_start[sc + 1];
+            }
+        }
+        if (!__any_sync(0xFFFFFFFFu, active)) break;
+        if (active) {
+            const float4 pj = __ldg(a.pos4 + j);
+            float dx = __fsub_rn(pi.x, pj.x);
+            float dy = __fsub_rn(pi.y, pj.y);
+            float dz = __fsub_rn(pi.z, pj.z);
+            if (anywrap) {
+                if (wfl & 1u) dx = min_image_f(dx, a.L[0], a.H[0]);
+                if (wfl & 2u) dy = min_image_f(dy, a.L[1], a.H[1]);
+                if (wfl & 4u) dz = min_image_f(dz, a.L[2], a.H[2]);
+            }
+            const float d2 =
+                __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
+            const bool hit = d2 <= a.cut_s && j != i;
+            if (hit) {
+                const bool core = d2 <= a.cut_c;
+                const bool front = WALK ? (j < fb0 || j > i) : core;
+                const uint32_t k = front ? kf : maxn - 1u - kb;
+                if (kf + kb < maxn)
+                    rowp[(k & 31u) * maxn + (k & ~31u)] = (WALK && !core) ? (j | 0x80000000u) : j;
+                kf += front;
+                kb += !front;
+                nc += core;
+                nsk += !core;
+            }
+            ++j;
+        }
+    }
+    if (row) {
+        if (nc + nsk > maxn)
+            raise_err(a.err, DPDB_EPHYSICS, EW_OVERFLOW, __float_as_uint(pi.w), nc + nsk);
+        const uint32_t ff = (fl >> 3) & 7u;
+        a.counts[i] = min(nc, 8191u) | (min(nsk, 8191u) << 13) | (ff << 26);
+        if (WALK) a.fwalk[i] = min(kf, maxn) | (ff << 26);
+    }
+}
+
 // layout transforms of the table
 __device__ __forceinline__ size_t raw_index(bool tiled, uint32_t maxn, uint32_t i, uint32_t k) {
     return tiled ? (size_t)((i & ~31u) + (k & 31u)) * maxn + (k & ~31u) + (i & 31u)
