@@ -433,9 +433,22 @@ void force_launch(dpdb_ctx* ctx, const dpdb::ForceArgs& a, bool body) {
         dpdb::k_force<MULTI, TILED, JOINED, false, WALK><<<nb, T, 0, ctx->stream>>>(a);
 }
 
+template <bool MULTI, bool BODY>
+void force_walk_launch(dpdb_ctx* ctx, const dpdb::ForceArgs& a) {
+    const unsigned nb = blocks_for(ctx->n, dpdb::FORCE_BLOCK);
+    constexpr int T = dpdb::FORCE_WARPS * 32;
+    if (ctx->maxn == 128)
+        dpdb::k_force_walk<MULTI, BODY, 128><<<nb, T, 0, ctx->stream>>>(a);
+    else
+        dpdb::k_force_walk<MULTI, BODY, 0><<<nb, T, 0, ctx->stream>>>(a);
+}
+
 template <bool MULTI>
 void force_dispatch_layout(dpdb_ctx* ctx, const dpdb::ForceArgs& a, bool body) {
-    if (ctx->walk) force_launch<MULTI, true, true, true>(ctx, a, body);
+    if (ctx->walk) {
+        if (body) force_walk_launch<MULTI, true>(ctx, a);
+        else force_walk_launch<MULTI, false>(ctx, a);
+    }
     else if (ctx->tiled && !ctx->joined) force_launch<MULTI, true, false>(ctx, a, body);
     else if (ctx->tiled) force_launch<MULTI, true, true>(ctx, a, body);
     else if (!ctx->joined) force_launch<MULTI, false, false>(ctx, a, body);

@@ -4,6 +4,7 @@
 //   compute_forces / dpd_pair_force   SPEC.md:425-442 (impl. not shipped)
 //   random term, RNG                  P:234-309, inc/rng.hpp:77-91
 #pragma once
+#include <type_traits>
 
 struct ForceArgs {
     const float4* pos4;
@@ -261,6 +262,222 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(ForceArgs a) {
             }
         }
         if (qtail > qhead) process(qhead, qtail - qhead);
+        __syncwarp();
+    }
+    if (coincident) raise_err(a.err, DPDB_EPHYSICS, EW_COINCIDENT, bad_tag, 0u);
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < bn; t += FORCE_WARPS * 32) {
+        const uint32_t i = b0 + t;
+        float fx = (float)acc[3 * t + 0] * FIX_INV;
+        float fy = (float)acc[3 * t + 1] * FIX_INV;
+        float fz = (float)acc[3 * t + 2] * FIX_INV;
+        if (BODY) {
+            const float g = a.xpart[i] < a.body_mid64 ? a.body_g : -a.body_g;
+            if (a.drive_axis == 0)
+                fx += g;
+            else if (a.drive_axis == 1)
+                fy += g;
+            else
+                fz += g;
+        }
+        a.f[0][i] = fx;
+        a.f[1][i] = fy;
+        a.f[2][i] = fz;
+    }
+}
+
+// Force kernel for the step pipeline's walk layout (k_build_lane<true> /
+// k_build<.., true>): same physics, pair set and fixed-point accumulation as
+// k_force, restructured so the per-candidate filter (phase A) is as cheap as
+// the hardware allows -- ~27 candidates are filtered per particle but only ~8
+// pairs evaluated, so phase A dominates the instruction count.
+//
+// Phase A (per candidate, per lane = row): one row-entry load and one pos4
+// load, fp32 distance, |r| <= r_c, a ballot, and one 4-byte shared store of
+// j | lane << 27 into the warp's pair queue.  Everything else the pair needs
+// (d, tags, in-block test, min-image) is recomputed in phase B, which runs
+// with all 32 lanes busy.  Row entries are fetched one group of 4 ahead with
+// compile-time strides (MAXN) and the 4 candidate positions of a group are
+// issued back to back, so each warp keeps up to 8 loads in flight without a
+// rotating register pipeline.  The queue (160 slots) is drained once per
+// group, in whole batches of 32.
+//
+// Each warp takes tiles (w, 15 - w) of the block: in-block pairs are taken by
+// the lower index, so early tiles carry more pairs; pairing them with late
+// tiles evens out the work before the block's final barrier.
+constexpr int FW_Q = 160;  // < 32 leftovers + 4 x 32 hits per group
+
+template <bool GENERAL, bool BODY, int MAXN>
+__global__ void __launch_bounds__(FORCE_WARPS * 32) k_force_walk(ForceArgs a) {
+    static_assert(FORCE_TILES == 2 * FORCE_WARPS, "tile pairing assumes 2 tiles per warp");
+    __shared__ uint32_t q_j[FORCE_WARPS][FW_Q];  // j | owner lane << 27
+    __shared__ float4 own_p[FORCE_WARPS][32];
+    __shared__ float4 own_v[FORCE_WARPS][32];
+    __shared__ uint32_t own_fl[FORCE_WARPS][32];
+    __shared__ int acc[FORCE_BLOCK * 3];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t b0 = blockIdx.x * FORCE_BLOCK;
+    const uint32_t bn = min((uint32_t)FORCE_BLOCK, a.n - b0);
+    for (int t = threadIdx.x; t < FORCE_BLOCK * 3; t += FORCE_WARPS * 32) acc[t] = 0;
+    __syncthreads();
+    const uint32_t lt = lanemask_lt();
+    const uint32_t maxn = MAXN ? (uint32_t)MAXN : a.maxn;
+    const uint32_t lanebits = (uint32_t)lane << 27;
+    bool coincident = false;
+    uint32_t bad_tag = 0;
+
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+        const uint32_t tile = pass ? (uint32_t)(FORCE_TILES - 1 - warp) : (uint32_t)warp;
+        const uint32_t il0 = 32u * tile;
+        if (il0 >= bn) continue;
+        const uint32_t il = il0 + lane;
+        const bool live = il < bn;
+        float4 pi = make_float4(0.f, 0.f, 0.f, 0.f), vi = pi;
+        uint32_t c = 0;
+        if (live) {
+            pi = a.pos4[b0 + il];
+            vi = a.vel4[b0 + il];
+            c = a.fwalk[b0 + il];
+        }
+        const uint32_t tot = c & 0x1FFFu, fl = c >> 26;
+        own_p[warp][lane] = pi;
+        own_v[warp][lane] = vi;
+        own_fl[warp][lane] = fl;
+        const uint32_t maxtot = __reduce_max_sync(0xFFFFFFFFu, tot);
+        const bool anywrap = __any_sync(0xFFFFFFFFu, fl != 0u);
+        __syncwarp();
+        uint32_t qtail = 0;
+
+        auto process = [&](uint32_t h, uint32_t cnt) {
+            if ((uint32_t)lane < cnt) {
+                const uint32_t jw = q_j[warp][h + lane];
+                const uint32_t o = jw >> 27, j = jw & 0x07FFFFFFu;
+                const float4 po = own_p[warp][o];
+                const float4 vo = own_v[warp][o];
+                const float4 pj = __ldg(a.pos4 + j);
+                const float4 vj = __ldg(a.vel4 + j);
+                float dx = po.x - pj.x, dy = po.y - pj.y, dz = po.z - pj.z;
+                if (anywrap) {
+                    const uint32_t f = own_fl[warp][o];
+                    if (f & 1u) dx = min_image_f(dx, a.L[0], a.H[0]);
+                    if (f & 2u) dy = min_image_f(dy, a.L[1], a.H[1]);
+                    if (f & 4u) dz = min_image_f(dz, a.L[2], a.H[2]);
+                }
+                uint32_t tag_i = __float_as_uint(po.w), tag_j = __float_as_uint(pj.w);
+                float ca = a.a, cg = a.gamma, cs = a.sigma_dt;
+                if (GENERAL && a.ns > 1) {  // species ride in the top 4 bits of the tag word
+                    const uint32_t q = (tag_i >> 28) * a.ns + (tag_j >> 28);
+                    ca = a.ta[q];
+                    cg = a.tg[q];
+                    cs = a.ts[q];
+                    tag_i &= 0x0FFFFFFFu;
+                    tag_j &= 0x0FFFFFFFu;
+                }
+                const uint32_t sig_i = __float_as_uint(vo.w), sig_j = __float_as_uint(vj.w);
+                const bool ifirst = tag_i < tag_j;
+                uint32_t u0 = ifirst ? sig_i : sig_j;
+                uint32_t u1 = (ifirst ? sig_j : sig_i) ^ a.step_mix;
+                tea4(u0, u1);
+                const float xi = gaussian_hot(u0, u1);
+                const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                if (r2 == 0.f) {
+                    coincident = true;
+                    bad_tag = tag_i;
+                }
+                const float rinv = rsqrt_ftz(r2);
+                const float w = fmaxf(fmaf(-r2 * rinv, a.inv_rc, 1.f), 0.f);
+                const float wr = GENERAL ? weight_pow_f(w, a.s_exp, a.smode) : w;
+                const float ev =
+                    (dx * (vo.x - vj.x) + dy * (vo.y - vj.y) + dz * (vo.z - vj.z)) * rinv;
+                const float mag =
+                    (ca * w - cg * (wr * wr) * ev + cs * wr * xi) * (rinv * FIX_SCALE);
+                const int qx = __float2int_rn(mag * dx);
+                const int qy = __float2int_rn(mag * dy);
+                const int qz = __float2int_rn(mag * dz);
+                int* ai = acc + 3 * (il0 + o);
+                atomicAdd(ai + 0, qx);
+                atomicAdd(ai + 1, qy);
+                atomicAdd(ai + 2, qz);
+                const uint32_t jl = j - b0;
+                if (jl < bn) {  // partner in this block (then j > i): it takes -q
+                    int* aj = acc + 3 * jl;
+                    atomicAdd(aj + 0, -qx);
+                    atomicAdd(aj + 1, -qy);
+                    atomicAdd(aj + 2, -qz);
+                }
+            }
+        };
+
+        // row position m of this lane: ep + (m & 31) * maxn + (m & ~31).
+        // Candidate positions are addressed as pos4 + (e << 4) bytes in 32-bit
+        // arithmetic, which drops the walk layout's skin tag (bit 31) for free
+        // (j < 2^26, so the byte offset fits in 32 bits).
+        const uint32_t* ep = a.entries + (size_t)(b0 + il0) * maxn + lane;
+        const char* pb = reinterpret_cast<const char*>(a.pos4);
+        uint32_t* qw = q_j[warp];
+        auto phase_a = [&](auto wrap_c) {
+            constexpr bool WRAP = decltype(wrap_c)::value;
+            uint32_t e[4] = {0u, 0u, 0u, 0u};
+            float4 p[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                p[k] = pi;
+                if ((uint32_t)k < tot) e[k] = __ldg(ep + k * maxn);
+            }
+            const float rc2 = a.rc2;
+#pragma unroll 1
+            for (uint32_t m0 = 0; m0 < maxtot; m0 += 4) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (m0 + k < tot)
+                        p[k] = __ldg(reinterpret_cast<const float4*>(pb + (e[k] << 4)));
+                uint32_t en[4] = {e[0], e[1], e[2], e[3]};
+                const uint32_t m1 = m0 + 4;
+                const uint32_t* gp = ep + (m1 & 31u) * maxn + (m1 & ~31u);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (m1 + k < tot) en[k] = __ldg(gp + k * maxn);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    float dx = pi.x - p[k].x, dy = pi.y - p[k].y, dz = pi.z - p[k].z;
+                    if (WRAP) {
+                        if (fl & 1u) dx = min_image_f(dx, a.L[0], a.H[0]);
+                        if (fl & 2u) dy = min_image_f(dy, a.L[1], a.H[1]);
+                        if (fl & 4u) dz = min_image_f(dz, a.L[2], a.H[2]);
+                    }
+                    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                    const bool hit = m0 + k < tot && r2 <= rc2;
+                    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, hit);
+                    if (hit) qw[qtail + __popc(bal & lt)] = (e[k] & 0x7FFFFFFFu) | lanebits;
+                    qtail += __popc(bal);
+                }
+                // drain whole batches, then move the (< 32) leftovers to the front
+                if (qtail >= 32u) {
+                    __syncwarp();
+                    uint32_t h = 0;
+                    do {
+                        process(h, 32u);
+                        h += 32u;
+                    } while (qtail - h >= 32u);
+                    __syncwarp();
+                    const uint32_t left = qtail - h;
+                    const uint32_t mv = (uint32_t)lane < left ? qw[h + lane] : 0u;
+                    __syncwarp();
+                    if ((uint32_t)lane < left) qw[lane] = mv;
+                    __syncwarp();
+                    qtail = left;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) e[k] = en[k];
+            }
+        };
+        if (anywrap)
+            phase_a(std::integral_constant<bool, true>{});
+        else
+            phase_a(std::integral_constant<bool, false>{});
+        __syncwarp();
+        if (qtail > 0) process(0u, qtail);
         __syncwarp();
     }
     if (coincident) raise_err(a.err, DPDB_EPHYSICS, EW_COINCIDENT, bad_tag, 0u);

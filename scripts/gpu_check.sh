@@ -1,9 +1,8 @@
+# GPU check: parity suite + bench (no CPU baseline) -- usage: bash scripts/gpu_check.sh TAG
 cd $GRAFT_REPO_ROOT
-nvidia-smi > gpurun_out/nvsmi.txt 2>&1
-timeout 1200 python -m pytest tests -q -m gpu --timeout 600 -p no:randomly > gpurun_out/pytest_gpu.txt 2>&1
-echo "pytest rc=$?" >> gpurun_out/pytest_gpu.txt
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1
-echo "smoke rc=$?" >> gpurun_out/smoke.txt
-timeout 600 python bench.py --steps 100 --warmup 10 > gpurun_out/bench.json 2> gpurun_out/bench.err
-echo "bench rc=$?" >> gpurun_out/bench.err
-tail -5 gpurun_out/pytest_gpu.txt; cat gpurun_out/smoke.txt; cat gpurun_out/bench.json; tail -5 gpurun_out/bench.err
+mkdir -p gpurun_out
+T=${1:-x}
+python -m pytest tests -m gpu -x -q 2>&1 | tail -8 > gpurun_out/pytest_$T.log
+cat gpurun_out/pytest_$T.log
+python bench.py --no-cpu-baseline > gpurun_out/bench_$T.json 2> gpurun_out/bench_$T.err
+python -c "import json;d=json.load(open('gpurun_out/bench_$T.json'));print(d['value'],d['stage_ms_per_step'],d['roofline']['frac'],d['e2e']['value'])" || tail -20 gpurun_out/bench_$T.err
