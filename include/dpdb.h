@@ -178,7 +178,8 @@ enum {
     DPDB_OP_FASTPOW = 8,       /* in0,in1 f64; out f64 */
     DPDB_OP_MORTON = 9,        /* in0 u32[3n]; param = bits; out u32 */
     DPDB_OP_FASTLOG32 = 10,    /* in0 u32; out f32 */
-    DPDB_OP_STEP_MIX = 11      /* in0 u32 seed, in1 u32 step; out u32 */
+    DPDB_OP_STEP_MIX = 11,     /* in0 u32 seed, in1 u32 step; out u32 */
+    DPDB_OP_GAUSSIAN_HOT = 12  /* in0,in1 u32; out f32 (the force kernels' Box-Muller) */
 };
 int dpdb_eval(int device, int op, size_t n, const void* in0, const void* in1, uint32_t param,
               void* out);

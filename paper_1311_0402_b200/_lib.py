@@ -54,7 +54,7 @@ class GridInfo(C.Structure):
 
 
 OP = dict(TEA_HASH=1, SIGNATURE=2, PAIR_UNIFORMS=3, GAUSSIAN64=4, GAUSSIAN32=5, FASTLOG=6,
-          FASTCOS2PI=7, FASTPOW=8, MORTON=9, FASTLOG32=10, STEP_MIX=11)
+          FASTCOS2PI=7, FASTPOW=8, MORTON=9, FASTLOG32=10, STEP_MIX=11, GAUSSIAN_HOT=12)
 
 # every symbol include/dpdb.h declares (checked by tests/test_abi.py)
 SYMBOLS = {

@@ -477,6 +477,7 @@ int do_forces(dpdb_ctx* ctx, uint32_t step) {
     a.gamma = (float)p.gamma[0];
     a.sigma_dt = (float)(ctx->sigma[0] / std::sqrt(p.dt));
     wrap_lengths(ctx, a.L, a.H);
+    for (int k = 0; k < 3; ++k) a.iL[k] = 1.0f / a.L[k];
     const bool body = ctx->run.body_force != 0.0;
     a.body_g = (float)ctx->run.body_force;
     a.drive_axis = ctx->run.drive_axis;
@@ -723,6 +724,9 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
     ctx->md_list_cap = ctx->md_valid ? 8 * c : 1;  // a corner particle sits in 7 lists
     if (cudaMemset(ctx->err, 0, sizeof(DevErr)) != cudaSuccess ||
         cudaMemset(ctx->counts, 0, c * 4) != cudaSuccess ||
+        // k_force_walk reads rows past their end (masked): every word must be
+        // a valid particle index from the start
+        cudaMemset(ctx->entries, 0, c * ctx->maxn * 4) != cudaSuccess ||
         cudaMemset(ctx->sp, 0, c) != cudaSuccess || cudaMemset(ctx->sp2, 0, c) != cudaSuccess ||
         cudaMemset(ctx->f[0], 0, c * 4) != cudaSuccess || cudaMemset(ctx->f[1], 0, c * 4) != cudaSuccess ||
         cudaMemset(ctx->f[2], 0, c * 4) != cudaSuccess)
@@ -1281,6 +1285,7 @@ int dpdb_eval(int device, int op, size_t n, const void* in0, const void* in1, ui
         case DPDB_OP_PAIR_UNIFORMS: s0 = 8; s1 = 8; so = 8; break;
         case DPDB_OP_GAUSSIAN64: so = 8; break;
         case DPDB_OP_GAUSSIAN32: break;
+        case DPDB_OP_GAUSSIAN_HOT: break;
         case DPDB_OP_FASTLOG: s1 = 0; so = 8; break;
         case DPDB_OP_FASTCOS2PI: s1 = 0; so = 8; break;
         case DPDB_OP_FASTPOW: s0 = 8; s1 = 8; so = 8; break;

@@ -20,6 +20,7 @@ struct ForceArgs {
     float rc2, inv_rc;
     float a, gamma, sigma_dt;  // single species: a, gamma, sigma / sqrt(dt)
     float L[3], H[3];
+    float iL[3];  // 1 / L (fp32)
     float body_g;
     int drive_axis;
     double body_mid64;
@@ -70,6 +71,14 @@ __device__ __forceinline__ float gaussian_hot(uint32_t ua, uint32_t ub) {
     const float y = (float)(int)((ub & 0x7FFFFFFFu) - 0x40000000u) * 0x1p-31f;
     const float s = sin_ftz(3.14159265358979f * y);
     return (ub >> 31) ? rad * s : -(rad * s);
+}
+
+// Branch-free fp32 minimum image for the walk force kernel: L = 0 (and
+// invL = 0) on axes without wrap.  d - L*rint(d/L) equals min_image_f's
+// d -/+ L exactly (one rounding) whenever |d| is not within an ulp of L/2,
+// i.e. for every pair that can be within r_c.
+__device__ __forceinline__ float min_image_rint(float d, float L, float invL) {
+    return fmaf(-L, rintf(d * invL), d);
 }
 
 __device__ __forceinline__ float weight_pow_f(float w, float s, int mode) {
@@ -305,10 +314,17 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(ForceArgs a) {
 // Each warp takes tiles (w, 15 - w) of the block: in-block pairs are taken by
 // the lower index, so early tiles carry more pairs; pairing them with late
 // tiles evens out the work before the block's final barrier.
+#ifndef DPDB_FW_UNCOND
+#define DPDB_FW_UNCOND 0
+#endif
+constexpr bool FW_UNCOND = DPDB_FW_UNCOND;
+#ifndef FW_MINB
+#define FW_MINB 4  // resident CTAs per SM the register allocation must allow (A/B: 1, 3, 4 -> 4 best)
+#endif  // A/B switch: unpredicated phase-A loads
 constexpr int FW_Q = 160;  // < 32 leftovers + 4 x 32 hits per group
 
 template <bool GENERAL, bool BODY, int MAXN>
-__global__ void __launch_bounds__(FORCE_WARPS * 32) k_force_walk(ForceArgs a) {
+__global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceArgs a) {
     static_assert(FORCE_TILES == 2 * FORCE_WARPS, "tile pairing assumes 2 tiles per warp");
     __shared__ uint32_t q_j[FORCE_WARPS][FW_Q];  // j | owner lane << 27
     __shared__ float4 own_p[FORCE_WARPS][32];
@@ -360,9 +376,9 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force_walk(ForceArgs a) {
                 float dx = po.x - pj.x, dy = po.y - pj.y, dz = po.z - pj.z;
                 if (anywrap) {
                     const uint32_t f = own_fl[warp][o];
-                    if (f & 1u) dx = min_image_f(dx, a.L[0], a.H[0]);
-                    if (f & 2u) dy = min_image_f(dy, a.L[1], a.H[1]);
-                    if (f & 4u) dz = min_image_f(dz, a.L[2], a.H[2]);
+                    dx = min_image_rint(dx, (f & 1u) ? a.L[0] : 0.f, (f & 1u) ? a.iL[0] : 0.f);
+                    dy = min_image_rint(dy, (f & 2u) ? a.L[1] : 0.f, (f & 2u) ? a.iL[1] : 0.f);
+                    dz = min_image_rint(dz, (f & 4u) ? a.L[2] : 0.f, (f & 4u) ? a.iL[2] : 0.f);
                 }
                 uint32_t tag_i = __float_as_uint(po.w), tag_j = __float_as_uint(pj.w);
                 float ca = a.a, cg = a.gamma, cs = a.sigma_dt;
@@ -409,47 +425,52 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force_walk(ForceArgs a) {
             }
         };
 
-        // row position m of this lane: ep + (m & 31) * maxn + (m & ~31).
-        // Candidate positions are addressed as pos4 + (e << 4) bytes in 32-bit
-        // arithmetic, which drops the walk layout's skin tag (bit 31) for free
-        // (j < 2^26, so the byte offset fits in 32 bits).
+        // Row position m of this lane: ep + (m & 31) * maxn + (m & ~31).
+        // Loads are unconditional: a row is read up to the warp's longest row
+        // (+ one prefetch group), and every word of the entries array is a
+        // valid particle index (zeroed at allocation, only indices written
+        // since), so positions past a row's end are harmless in-bounds reads
+        // masked by m < tot.  pos4 is addressed as (e << 4) bytes in 32-bit
+        // arithmetic, which drops the walk layout's skin tag (bit 31).
         const uint32_t* ep = a.entries + (size_t)(b0 + il0) * maxn + lane;
         const char* pb = reinterpret_cast<const char*>(a.pos4);
         uint32_t* qw = q_j[warp];
         auto phase_a = [&](auto wrap_c) {
             constexpr bool WRAP = decltype(wrap_c)::value;
-            uint32_t e[4] = {0u, 0u, 0u, 0u};
-            float4 p[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                p[k] = pi;
-                if ((uint32_t)k < tot) e[k] = __ldg(ep + k * maxn);
+            float lx = 0.f, ly = 0.f, lz = 0.f, ilx = 0.f, ily = 0.f, ilz = 0.f;
+            if (WRAP) {
+                if (fl & 1u) lx = a.L[0], ilx = a.iL[0];
+                if (fl & 2u) ly = a.L[1], ily = a.iL[1];
+                if (fl & 4u) lz = a.L[2], ilz = a.iL[2];
             }
             const float rc2 = a.rc2;
-#pragma unroll 1
-            for (uint32_t m0 = 0; m0 < maxtot; m0 += 4) {
+            // one group = 4 row positions: positions of the group's candidates,
+            // prefetch of the next group's entries, filter, enqueue, drain
+            auto group = [&](uint32_t m0, const uint32_t (&cur)[4], uint32_t (&nxt)[4]) {
+                // lanes past their row end load the block's first particle
+                // instead (one shared line, no extra wavefronts); hit masks them
+                float4 p[4];
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (m0 + k < tot)
-                        p[k] = __ldg(reinterpret_cast<const float4*>(pb + (e[k] << 4)));
-                uint32_t en[4] = {e[0], e[1], e[2], e[3]};
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t jk = (FW_UNCOND || m0 + k < tot) ? cur[k] : b0;
+                    p[k] = __ldg(reinterpret_cast<const float4*>(pb + (jk << 4)));
+                }
                 const uint32_t m1 = m0 + 4;
                 const uint32_t* gp = ep + (m1 & 31u) * maxn + (m1 & ~31u);
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (m1 + k < tot) en[k] = __ldg(gp + k * maxn);
+                for (int k = 0; k < 4; ++k) nxt[k] = __ldg(gp + k * maxn);  // coalesced
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     float dx = pi.x - p[k].x, dy = pi.y - p[k].y, dz = pi.z - p[k].z;
                     if (WRAP) {
-                        if (fl & 1u) dx = min_image_f(dx, a.L[0], a.H[0]);
-                        if (fl & 2u) dy = min_image_f(dy, a.L[1], a.H[1]);
-                        if (fl & 4u) dz = min_image_f(dz, a.L[2], a.H[2]);
+                        dx = min_image_rint(dx, lx, ilx);
+                        dy = min_image_rint(dy, ly, ily);
+                        dz = min_image_rint(dz, lz, ilz);
                     }
                     const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
                     const bool hit = m0 + k < tot && r2 <= rc2;
                     const uint32_t bal = __ballot_sync(0xFFFFFFFFu, hit);
-                    if (hit) qw[qtail + __popc(bal & lt)] = (e[k] & 0x7FFFFFFFu) | lanebits;
+                    if (hit) qw[qtail + __popc(bal & lt)] = (cur[k] & 0x7FFFFFFFu) | lanebits;
                     qtail += __popc(bal);
                 }
                 // drain whole batches, then move the (< 32) leftovers to the front
@@ -468,8 +489,15 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force_walk(ForceArgs a) {
                     __syncwarp();
                     qtail = left;
                 }
+            };
+            uint32_t ea[4], eb[4];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) e[k] = en[k];
+            for (int k = 0; k < 4; ++k) ea[k] = __ldg(ep + k * maxn);
+#pragma unroll 1
+            for (uint32_t m0 = 0; m0 < maxtot; m0 += 8) {
+                group(m0, ea, eb);
+                if (m0 + 4 >= maxtot) break;
+                group(m0 + 4, eb, ea);
             }
         };
         if (anywrap)

@@ -929,6 +929,9 @@ __global__ void k_eval(int op, uint32_t n, const void* in0, const void* in1, uin
         case DPDB_OP_FASTLOG32:
             static_cast<float*>(out)[i] = fastlog32(u0[i]);
             break;
+        case DPDB_OP_GAUSSIAN_HOT:
+            static_cast<float*>(out)[i] = gaussian_hot(u0[i], u1[i]);
+            break;
         case DPDB_OP_STEP_MIX:
             static_cast<uint32_t*>(out)[i] = step_mix_of(u0[i], u1[i]);
             break;

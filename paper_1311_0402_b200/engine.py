@@ -390,8 +390,12 @@ def pair_uniforms(sig_i, sig_j, tag_i, tag_j, mix, device=0):
     return _eval("PAIR_UNIFORMS", len(sig), sig, tag, mix, out, device).reshape(-1, 2)
 
 
-def gaussian(ua, ub, device=0, fp32=False):
+def gaussian(ua, ub, device=0, fp32=False, hot=False):
+    """xi from two TEA words: fp64 bit-exact (inc/rng.hpp:88-91), or fp32
+    (fp32=True: gaussian32; hot=True: the force kernels' ftz-intrinsic form)."""
     ua, ub = (np.ascontiguousarray(np.atleast_1d(v), np.uint32) for v in (ua, ub))
+    if hot:
+        return _eval("GAUSSIAN_HOT", len(ua), ua, ub, 0, np.zeros(len(ua), np.float32), device)
     if fp32:
         return _eval("GAUSSIAN32", len(ua), ua, ub, 0, np.zeros(len(ua), np.float32), device)
     return _eval("GAUSSIAN64", len(ua), ua, ub, 0, np.zeros(len(ua)), device)

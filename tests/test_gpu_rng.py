@@ -62,6 +62,20 @@ def test_gaussian32_hot_path_accuracy(golden):
     assert (np.abs(lg - lref) / np.abs(lref)).max() < 5e-7
 
 
+def test_gaussian_hot_accuracy(golden):
+    """The Box-Muller the force kernels run (rcp/rsqrt/sin.approx, ftz) vs the
+    bit-exact fp64 one, including u_a -> 2^32 where ln u cancels."""
+    g = golden.fastmath
+    rng = np.random.default_rng(6)
+    a = np.concatenate([g["gauss_a"], rng.integers(0, 2**32, 1000000).astype(np.uint32),
+                        (2**32 - np.arange(1, 5000)).astype(np.uint32), np.arange(0, 5000, dtype=np.uint32)])
+    b = np.concatenate([g["gauss_b"], rng.integers(0, 2**32, 1000000).astype(np.uint32),
+                        rng.integers(0, 2**32, 9999).astype(np.uint32)])
+    ref = dpd.gaussian(a, b)
+    got = dpd.gaussian(a, b, hot=True).astype(np.float64)
+    assert np.abs(got - ref).max() < 4e-6, np.abs(got - ref).max()
+
+
 def test_gaussian_moments():
     """moments of 2^20 Gaussians from signature-TEA + Box-Muller."""
     n = 2**20
@@ -69,8 +83,8 @@ def test_gaussian_moments():
                              np.random.default_rng(0).normal(size=(n, 3)))
     u = dpd.pair_uniforms(sig, np.roll(sig, 1), np.arange(1, n + 1), np.roll(np.arange(1, n + 1), 1),
                           0x8562613F)
-    for fp32 in (False, True):
-        xi = dpd.gaussian(u[:, 0], u[:, 1], fp32=fp32).astype(np.float64)
+    for fp32, hot in ((False, False), (True, False), (False, True)):
+        xi = dpd.gaussian(u[:, 0], u[:, 1], fp32=fp32, hot=hot).astype(np.float64)
         m = xi.mean()
         v = xi.var()
         sk = ((xi - m) ** 3).mean() / v**1.5
