@@ -53,11 +53,16 @@ struct dpdb_ctx {
     float4 *pos4{}, *vel4{};
     uint32_t *keys{}, *keys2{}, *vals{}, *vals2{}, *hist{};
     uint32_t *cell_start{}, *rank_of_cell{}, *stencil{};
-    uint8_t *stencil_n{}, *cell_flags{};
+    uint8_t *stencil_n{}, *cell_flags{}, *stencil_code{};
+    float4* cell_lo{};
     uint32_t *entries{}, *counts{}, *fwalk{};
     uint2* rowmeta{};
-    int walk = 0;         // table layout: 0 reference (split/joined), 1 ballot walk (k_build), 2 lane walk (k_build_lane)
-    bool lane_builder = true;  // k_build_lane (default) or the ballot k_build (DPDB_BUILDER=ballot)
+    // table layout: 0 reference (split/joined), 1 ballot walk (k_build), 2 lane
+    // walk (k_build_lane), 3 range walk (k_build_range: front entries only)
+    int walk = 0;
+    // builder: 2 = k_build_range (default), 1 = k_build_lane (DPDB_BUILDER=lane),
+    // 0 = the ballot k_build (DPDB_BUILDER=ballot)
+    int builder = 2;
     DevErr* err{};
     double *red{}, *red_out{};
     uint32_t* tmp_u32{};
@@ -365,7 +370,7 @@ int do_build(dpdb_ctx* ctx, bool joined_out) {
     if (!ctx->have_sorted) return fail(ctx, DPDB_ECONFIG, "build_neighbor_table: particles not reordered");
     ctx->tiled = true;
     ctx->joined = joined_out;
-    ctx->walk = joined_out ? (ctx->lane_builder ? 2 : 1) : 0;
+    ctx->walk = joined_out ? (ctx->builder == 2 ? 3 : ctx->builder == 1 ? 2 : 1) : 0;
     ctx->have_table = true;
     if (!ctx->n) return 0;
     dpdb::BuildArgs a{};
@@ -389,7 +394,22 @@ int do_build(dpdb_ctx* ctx, bool joined_out) {
     a.cut_c = (float)(rc * rc);
     a.cut_s = (float)(rs * rs);
     wrap_lengths(ctx, a.L, a.H);
-    if (ctx->lane_builder) {
+    if (ctx->builder == 2) {
+        a.stencil_code = ctx->stencil_code;
+        a.cell_lo = ctx->cell_lo;
+        for (int k = 0; k < 3; ++k) a.csz[k] = (float)ctx->grid.cell_size[k];
+        const double rm = rs + 1e-3;  // margin over the fp32 frame's rounding
+        a.cut_cull = (float)(rm * rm);
+        const unsigned nb = (unsigned)((ctx->n + dpdb::RB_BLOCK - 1) / dpdb::RB_BLOCK);
+        if (joined_out)
+            dpdb::k_build_range<true><<<nb, dpdb::RB_THREADS, dpdb::RB_SMEM, ctx->stream>>>(a);
+        else
+            dpdb::k_build_range<false><<<nb, dpdb::RB_THREADS, dpdb::RB_SMEM, ctx->stream>>>(a);
+        CKL();
+        ctx->launches[ST_BUILD]++;
+        return 0;
+    }
+    if (ctx->builder == 1) {
         if (joined_out)
             dpdb::k_build_lane<true><<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(a);
         else
@@ -634,7 +654,8 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
     ctx->params = *params;
     ctx->run = *run;
     ctx->maxn = run->max_neighbors;
-    if (const char* b = std::getenv("DPDB_BUILDER")) ctx->lane_builder = std::strcmp(b, "ballot") != 0;
+    if (const char* b = std::getenv("DPDB_BUILDER"))
+        ctx->builder = !std::strcmp(b, "ballot") ? 0 : !std::strcmp(b, "lane") ? 1 : 2;
     ctx->multi = params->n_species > 1;
     for (int q = 0; q < ns * ns; ++q) ctx->sigma[q] = std::sqrt(2.0 * params->gamma[q] * params->kbt);
     std::string err;
@@ -711,6 +732,8 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         (rc = dalloc(ctx, ctx->stencil, (size_t)g.n_local_cells * 32)) ||
         (rc = dalloc(ctx, ctx->stencil_n, (size_t)g.n_local_cells)) ||
         (rc = dalloc(ctx, ctx->cell_flags, (size_t)g.n_local_cells)) ||
+        (rc = dalloc(ctx, ctx->stencil_code, (size_t)g.n_local_cells * 32)) ||
+        (rc = dalloc(ctx, ctx->cell_lo, (size_t)g.n_local_cells)) ||
         (rc = dalloc(ctx, ctx->entries, c * ctx->maxn)) || (rc = dalloc(ctx, ctx->counts, c)) ||
         (rc = dalloc(ctx, ctx->fwalk, c)) || (rc = dalloc(ctx, ctx->rowmeta, c)) ||
         (rc = dalloc(ctx, ctx->md_masks, c)) || (rc = dalloc(ctx, ctx->md_mig, c)) ||
@@ -732,9 +755,12 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         cudaMemset(ctx->f[2], 0, c * 4) != cudaSuccess)
         return bail(fail(ctx, DPDB_EDEVICE, "cudaMemset"));
     std::vector<uint32_t> rows;
-    std::vector<uint8_t> cnt, flags;
-    g.coarse_stencil(rows, cnt, flags);
-    if (cudaMemcpy(ctx->rank_of_cell, g.rank_of_cell.data(), g.rank_of_cell.size() * 4,
+    std::vector<uint8_t> cnt, flags, codes;
+    std::vector<float> clo;
+    g.coarse_stencil(rows, cnt, flags, &codes, &clo);
+    if (cudaMemcpy(ctx->stencil_code, codes.data(), codes.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(ctx->cell_lo, clo.data(), clo.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(ctx->rank_of_cell, g.rank_of_cell.data(), g.rank_of_cell.size() * 4,
                    cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(ctx->stencil, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(ctx->stencil_n, cnt.data(), cnt.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -746,6 +772,11 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         cudaFuncSetAttribute(dpdb::k_build<BUILD_WARPS, BUILD_TILES, false>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return bail(fail(ctx, DPDB_ECONFIG, "max_neighbors too large for the builder's shared memory"));
+    if (cudaFuncSetAttribute(dpdb::k_build_range<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)dpdb::RB_SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(dpdb::k_build_range<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)dpdb::RB_SMEM) != cudaSuccess)
+        return bail(fail(ctx, DPDB_EDEVICE, "range builder shared memory"));
     *out = ctx;
     return 0;
 }
@@ -758,7 +789,7 @@ int dpdb_destroy(dpdb_ctx* ctx) {
     void* ptrs[] = {ctx->tag, ctx->tag2, ctx->mol, ctx->mol2, ctx->sp, ctx->sp2, ctx->pos4,
                     ctx->vel4, ctx->keys, ctx->keys2, ctx->vals, ctx->vals2, ctx->hist,
                     ctx->cell_start, ctx->rank_of_cell, ctx->stencil, ctx->stencil_n,
-                    ctx->cell_flags, ctx->entries, ctx->counts, ctx->fwalk, ctx->rowmeta,
+                    ctx->cell_flags, ctx->stencil_code, ctx->cell_lo, ctx->entries, ctx->counts, ctx->fwalk, ctx->rowmeta,
                     ctx->err, ctx->red, ctx->red_out,
                     ctx->tmp_u32, ctx->bond_off, ctx->bond_partner, ctx->index_of_tag,
                     ctx->bond_k, ctx->bond_r0, ctx->md_masks, ctx->md_mig, ctx->md_slot,
@@ -1043,7 +1074,20 @@ int unwalk(dpdb_ctx* ctx) {
     CK(cudaMemcpy(raw.data(), ctx->entries, raw.size() * 4, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(cnt.data(), ctx->counts, n * 4, cudaMemcpyDeviceToHost));
     if (layout == 1) CK(cudaMemcpy(meta.data(), ctx->rowmeta, n * sizeof(uint2), cudaMemcpyDeviceToHost));
-    if (layout == 2) CK(cudaMemcpy(fw.data(), ctx->fwalk, n * 4, cudaMemcpyDeviceToHost));
+    if (layout >= 2) CK(cudaMemcpy(fw.data(), ctx->fwalk, n * 4, cudaMemcpyDeviceToHost));
+    // layout 3 keeps only the front entries: the in-block j < i entries of row
+    // i are the transposes of front entries (j -> i, j > i, same force block)
+    std::vector<std::vector<uint32_t>> extra(layout == 3 ? n : 0);
+    if (layout == 3)
+        for (size_t i = 0; i < n; ++i) {
+            const uint32_t nf = std::min<uint32_t>(fw[i] & 0x1FFFu, (uint32_t)maxn);
+            for (uint32_t k = 0; k < nf; ++k) {
+                const uint32_t e = raw[((i & ~size_t(31)) + (k & 31)) * maxn + (k & ~size_t(31)) + (i & 31)];
+                const size_t j = e & 0x7FFFFFFFu;
+                if (j > i && j < n && j / dpdb::FORCE_BLOCK == i / dpdb::FORCE_BLOCK)
+                    extra[j].push_back((uint32_t)i | (e & 0x80000000u));
+            }
+        }
     auto idx = [&](size_t i, size_t k) { return ((i & ~size_t(31)) + (k & 31)) * maxn + (k & ~size_t(31)) + (i & 31); };
     std::vector<uint32_t> row(maxn), core, skin;
     for (size_t i = 0; i < n; ++i) {
@@ -1066,7 +1110,10 @@ int unwalk(dpdb_ctx* ctx) {
             skin.clear();
             auto put = [&](uint32_t e) { (e >> 31 ? skin : core).push_back(e & 0x7FFFFFFFu); };
             for (uint32_t k = 0; k < nf; ++k) put(raw[idx(i, k)]);
-            for (uint32_t q = 0; q < nb; ++q) put(raw[idx(i, maxn - 1 - q)]);
+            if (layout == 2)
+                for (uint32_t q = 0; q < nb; ++q) put(raw[idx(i, maxn - 1 - q)]);
+            else
+                for (uint32_t e : extra[i]) put(e);
             std::sort(core.begin(), core.end());
             std::sort(skin.begin(), skin.end());
             for (uint32_t e : core) row[w++] = e;
@@ -1342,3 +1389,4 @@ int dpdb_radix_sort(int device, uint32_t* keys, uint32_t* vals, size_t n, int bi
 }  // extern "C"
 
 #include "domain_host.inc"
+static_assert(dpdb::RB_BLOCK == dpdb::FORCE_BLOCK, "range builder CTA must own one force block");

@@ -135,15 +135,33 @@ struct HostGrid {
     //             interior cell could see |dx| >= L/2)
     //   bits 3-5: the force kernel must (3 cell layers from the seam, or
     //             ncell_k < 8, covering drift between rebuilds)
+    //
+    // codes (optional, k_build_range's cell culling): per stencil slot the
+    // offset (ox+1) | (oy+1) << 2 | (oz+1) << 4 of that cell from the centre
+    // cell, or 0xFF (never cull) when the slot stands for several offsets (deduplicated
+    // small grids) or a wrapped axis has < 5 cells (the nearest image need not
+    // be the geometric neighbor); cell_lo: each local cell's lower corner in
+    // the pos4 frame (x - slab centre), fp32.
     void coarse_stencil(std::vector<uint32_t>& rows, std::vector<uint8_t>& counts,
-                        std::vector<uint8_t>& flags) const {
+                        std::vector<uint8_t>& flags, std::vector<uint8_t>* codes = nullptr,
+                        std::vector<float>* cell_lo = nullptr) const {
         rows.assign((size_t)n_local_cells * 32, 0);
         counts.assign(n_local_cells, 0);
         flags.assign(n_local_cells, 0);
+        bool cull = true;
+        for (int k = 0; k < 3; ++k)
+            if (wrap[k] && ncell[k] < 5) cull = false;
+        if (codes) codes->assign((size_t)n_local_cells * 32, 0xFF);
+        if (cell_lo) cell_lo->assign((size_t)n_local_cells * 4, 0.f);
         for (uint32_t r = 0; r < n_local_cells; ++r) {
             int c[3];
             ext_coords(cell_of_rank[r], c);
+            if (cell_lo)
+                for (int k = 0; k < 3; ++k)
+                    (*cell_lo)[(size_t)r * 4 + k] =
+                        (float)(origin[k] + c[k] * cell_size[k] - 0.5 * (slab_lo[k] + slab_hi[k]));
             uint32_t list[27];
+            std::pair<uint32_t, int> coded[27];
             int m = 0;
             for (int dz = -1; dz <= 1; ++dz)
                 for (int dy = -1; dy <= 1; ++dy)
@@ -159,12 +177,20 @@ struct HostGrid {
                                 ok = false;
                             nc[k] = v;
                         }
-                        if (ok) list[m++] = rank_of_cell[ext_index(nc)];
+                        if (ok) {
+                            coded[m] = {rank_of_cell[ext_index(nc)], (dx + 1) | (dy + 1) << 2 | (dz + 1) << 4};
+                            list[m] = coded[m].first;
+                            ++m;
+                        }
                     }
             std::sort(list, list + m);
             const int u = (int)(std::unique(list, list + m) - list);
             std::copy(list, list + u, rows.begin() + (size_t)r * 32);
             counts[r] = (uint8_t)u;
+            if (codes && cull && u == m) {
+                std::sort(coded, coded + m);
+                for (int q = 0; q < m; ++q) (*codes)[(size_t)r * 32 + q] = (uint8_t)coded[q].second;
+            }
             uint8_t f = 0;
             for (int k = 0; k < 3; ++k) {
                 if (!wrap[k]) continue;

@@ -444,6 +444,11 @@ struct BuildArgs {
     int key_shift;
     float cut_c, cut_s;
     float L[3], H[3];
+    // k_build_range only: per-slot stencil offset codes and the cell boxes
+    const uint8_t* stencil_code;  // [n_local_cells][32]: (ox+1) | (oy+1) << 2 | (oz+1) << 4, 0xFF = never cull
+    const float4* cell_lo;        // [n_local_cells]: lower corner in the pos4 frame
+    float csz[3];                 // cell side per axis (fp32)
+    float cut_cull;               // (r_c + skin + margin)^2
 };
 
 // fp32 minimum image, src/core.cpp:129-139 semantics with L, L/2 in fp32
@@ -745,6 +750,226 @@ __global__ void __launch_bounds__(256) k_build_lane(BuildArgs a) {
         const uint32_t ff = (fl >> 3) & 7u;
         a.counts[i] = min(nc, 8191u) | (min(nsk, 8191u) << 13) | (ff << 26);
         if (WALK) a.fwalk[i] = min(kf, maxn) | (ff << 26);
+    }
+}
+
+// Range-list ordered builder (same rows as k_build_lane, bit for bit); the
+// step pipeline's default.  One CTA of RB_THREADS lanes owns one force block
+// of RB_BLOCK rows and takes it in RB_BLOCK / RB_THREADS passes (lane = row).
+// Per row, two phases:
+//
+//  1. Ranges.  The lane walks its <= 27 stencil cells in ascending rank
+//     order, drops the cells whose box lies farther than r_c + skin from its
+//     own position (conservative point-to-box distance with a 1e-3 margin, so
+//     no cell holding a hit is ever dropped; off when a wrapped axis has < 5
+//     cells), cuts out the index range it must not test -- itself, and in the
+//     walk layout the in-block j < i (that pair belongs to row j) -- and
+//     stores the surviving contiguous index ranges in shared memory
+//     (slot-major, bank-conflict free).  The ranges stay ascending, so the
+//     row stays ordered.
+//  2. Walk.  The lane tests its candidates range after range with one
+//     position load, the oracle's fp32 distance and one compare each.  A
+//     cursor runs two candidates ahead of the test (two position loads in
+//     flight per lane); moving to the next range is two shared loads, so
+//     lanes never diverge on cell switches.  Hits are stored straight into
+//     the 32x32 tile-transposed layout (raw_index).  No atomics and no sort
+//     for the rows.
+//
+// !WALK: the reference split layout (core from the front, skin reversed from
+//        the back), counts = core | skin << 13 | flags << 26.
+//  WALK: only the entries the force kernel evaluates (j outside the block or
+//        j > i), ascending, skin tagged with bit 31; fwalk = n_front | flags.
+//        The in-block j < i entries are not stored -- they are exactly the
+//        transposes of the block's front entries (unwalk restores them) --
+//        but they are counted (shared-memory integer adds, order-free) so
+//        counts and the overflow check equal the reference's full rows.
+constexpr int RB_BLOCK = 512;    // == FORCE_BLOCK (force.cuh)
+constexpr int RB_THREADS = 256;
+constexpr int RB_SLOTS = 29;     // 27 stencil cells + one split by the cut-out + a trash slot
+constexpr size_t RB_SMEM = (size_t)RB_SLOTS * RB_THREADS * 6 + RB_BLOCK * 4;
+constexpr uint32_t RB_NONE = 0xFFFFFFFFu;
+
+template <bool WALK>
+__global__ void __launch_bounds__(RB_THREADS, 4) k_build_range(BuildArgs a) {
+    extern __shared__ uint32_t rb_smem[];  // RB_SMEM bytes (dynamic: > 48 KB)
+    uint32_t(*rs)[RB_THREADS] = reinterpret_cast<uint32_t(*)[RB_THREADS]>(rb_smem);
+    uint16_t(*rl)[RB_THREADS] =
+        reinterpret_cast<uint16_t(*)[RB_THREADS]>(rb_smem + RB_SLOTS * RB_THREADS);
+    uint32_t* back = rb_smem + RB_SLOTS * RB_THREADS + RB_SLOTS * RB_THREADS / 2;
+    const uint32_t t = threadIdx.x;
+    const uint32_t b0 = blockIdx.x * RB_BLOCK;
+    const uint32_t bn = min((uint32_t)RB_BLOCK, a.n_local - b0);
+    const uint32_t bend = b0 + bn;
+    const uint32_t maxn = a.maxn;
+    if (WALK)
+        for (uint32_t q = t; q < RB_BLOCK; q += RB_THREADS) back[q] = 0;
+    __syncthreads();
+    uint32_t cnt[RB_BLOCK / RB_THREADS];  // nc | nsk << 16 per pass
+    uint32_t kfs[RB_BLOCK / RB_THREADS];
+
+#pragma unroll 1
+    for (int pass = 0; pass < RB_BLOCK / RB_THREADS; ++pass) {
+        const uint32_t i = b0 + pass * RB_THREADS + t;
+        const bool row = i < bend;
+        uint32_t r = 0, ns = 0, fl = 0;
+        float4 pi = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row) {
+            r = min(a.keys[i] >> a.key_shift, a.n_local_cells - 1u);
+            ns = a.stencil_n[r];
+            fl = a.cell_flags[r];
+            pi = a.pos4[i];
+        }
+        // ---- phase 1: ranges
+        float dm[3], dp[3];  // squared distance to the offset -1 / +1 slabs per axis
+        {
+            const float4 lo = row ? a.cell_lo[r] : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float l[3] = {pi.x - lo.x, pi.y - lo.y, pi.z - lo.z};
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const float m = fmaxf(l[k], 0.f), p = fmaxf(a.csz[k] - l[k], 0.f);
+                dm[k] = m * m;
+                dp[k] = p * p;
+            }
+        }
+        const uint32_t cut_lo = WALK ? b0 : i;  // excluded index range [cut_lo, i]
+        uint32_t nr = 0;
+        const uint32_t* srow = a.stencil + (size_t)r * 32;
+        const uint8_t* crow = a.stencil_code + (size_t)r * 32;
+        bool big = false;
+#pragma unroll 1
+        for (uint32_t s0 = 0; s0 < ns; s0 += 4) {
+            uint32_t sc[4], cd[4], st[4], en[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const bool v = s0 + q < ns;
+                sc[q] = v ? srow[s0 + q] : 0u;
+                cd[q] = v ? crow[s0 + q] : 0u;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                st[q] = a.cell_start[sc[q]];
+                en[q] = a.cell_start[sc[q] + 1];
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                // branch-free: both pieces are always written, nr advances only
+                // over the kept non-empty ones (slot RB_SLOTS - 1 absorbs the rest)
+                const uint32_t c = cd[q];
+                float d2 = 0.f;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const uint32_t o = (c >> (2 * k)) & 3u;
+                    const float v = (o & 2u) ? dp[k] : dm[k];
+                    d2 += (o & 1u) ? 0.f : v;
+                }
+                const bool keep = s0 + q < ns && (c == 0xFFu || d2 <= a.cut_cull);
+                const uint32_t e1 = min(en[q], cut_lo), s2 = max(st[q], i + 1u);
+                const uint32_t l1 = e1 > st[q] ? e1 - st[q] : 0u;
+                const uint32_t l2 = en[q] > s2 ? en[q] - s2 : 0u;
+                big |= keep && max(l1, l2) > 0xFFFFu;
+                rs[nr][t] = st[q];
+                rl[nr][t] = (uint16_t)min(l1, 0xFFFFu);
+                nr += keep && l1;
+                rs[nr][t] = s2;
+                rl[nr][t] = (uint16_t)min(l2, 0xFFFFu);
+                nr += keep && l2;
+            }
+        }
+        if (big) raise_err(a.err, DPDB_EPHYSICS, EW_OVERFLOW, __float_as_uint(pi.w), 0xFFFFu);
+        // ---- phase 2: walk the ranges, cursor two candidates ahead.  Written
+        // branch-light: lanes past their last candidate keep testing their own
+        // position (masked by v), and the range switch is a predicated pair of
+        // shared loads.
+        const uint32_t wfl = fl & 7u;
+        const bool anywrap = __any_sync(0xFFFFFFFFu, wfl != 0u);
+        uint32_t cs = 0, cj = 0, ce = 0;  // cursor: range, next index, range end
+        if (nr) {
+            cj = rs[0][t];
+            ce = cj + rl[0][t];
+        }
+        uint32_t j0, j1;
+        bool v0, v1;
+        auto adv = [&](uint32_t& j, bool& v) {
+            v = cj < ce;
+            if (!v && cs + 1 < nr) {
+                ++cs;
+                cj = rs[cs][t];
+                ce = cj + rl[cs][t];
+                v = true;
+            }
+            j = v ? cj : i;
+            cj += v;
+        };
+        adv(j0, v0);
+        adv(j1, v1);
+        float4 p0 = __ldg(a.pos4 + j0), p1 = __ldg(a.pos4 + j1);
+        uint32_t* rowp = a.entries + (size_t)(i & ~31u) * maxn + (i & 31u);
+        uint32_t kf = 0, kb = 0, nc = 0, nsk = 0;
+        const float cut_s = a.cut_s, cut_c = a.cut_c;
+        // branch-free min image (min_image_f semantics): axes without wrap get
+        // H = +inf, so neither correction fires
+        const float inf = __int_as_float(0x7F800000);
+        const float Lx = a.L[0], Ly = a.L[1], Lz = a.L[2];
+        const float Hx = (wfl & 1u) ? a.H[0] : inf, Hy = (wfl & 2u) ? a.H[1] : inf,
+                    Hz = (wfl & 4u) ? a.H[2] : inf;
+        auto mimg = [](float d, float L, float H) {
+            const float lo = __fsub_rn(d, L), hi = __fadd_rn(d, L);
+            return d >= H ? lo : (d < -H ? hi : d);
+        };
+        auto test = [&](uint32_t j, float4 pj, bool v) {
+            float dx = __fsub_rn(pi.x, pj.x);
+            float dy = __fsub_rn(pi.y, pj.y);
+            float dz = __fsub_rn(pi.z, pj.z);
+            if (anywrap) {
+                dx = mimg(dx, Lx, Hx);
+                dy = mimg(dy, Ly, Hy);
+                dz = mimg(dz, Lz, Hz);
+            }
+            const float d2 =
+                __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
+            const bool hit = v && d2 <= cut_s;
+            const bool core = d2 <= cut_c;
+            if (WALK) {
+                if (hit && kf < maxn) rowp[(kf & 31u) * maxn + (kf & ~31u)] = core ? j : (j | 0x80000000u);
+                kf += hit;
+                if (hit && j < bend && j > i) atomicAdd(&back[j - b0], core ? 1u : 0x10000u);
+            } else {
+                const uint32_t k = core ? kf : maxn - 1u - kb;
+                if (hit && kf + kb < maxn) rowp[(k & 31u) * maxn + (k & ~31u)] = j;
+                kf += hit && core;
+                kb += hit && !core;
+            }
+            nc += hit && core;
+            nsk += hit && !core;
+        };
+        while (__any_sync(0xFFFFFFFFu, v0)) {
+            test(j0, p0, v0);
+            adv(j0, v0);
+            p0 = __ldg(a.pos4 + j0);
+            test(j1, p1, v1);
+            adv(j1, v1);
+            p1 = __ldg(a.pos4 + j1);
+        }
+        cnt[pass] = nc | (nsk << 16);
+        kfs[pass] = kf;
+    }
+    if (WALK) __syncthreads();
+#pragma unroll
+    for (int pass = 0; pass < RB_BLOCK / RB_THREADS; ++pass) {
+        const uint32_t i = b0 + pass * RB_THREADS + t;
+        if (i >= bend) break;
+        uint32_t nc = cnt[pass] & 0xFFFFu, nsk = cnt[pass] >> 16;
+        if (WALK) {
+            const uint32_t bk = back[i - b0];
+            nc += bk & 0xFFFFu;
+            nsk += bk >> 16;
+        }
+        const uint32_t r = min(a.keys[i] >> a.key_shift, a.n_local_cells - 1u);
+        const uint32_t ff = (a.cell_flags[r] >> 3) & 7u;
+        if (nc + nsk > maxn)
+            raise_err(a.err, DPDB_EPHYSICS, EW_OVERFLOW, __float_as_uint(a.pos4[i].w), nc + nsk);
+        a.counts[i] = min(nc, 8191u) | (min(nsk, 8191u) << 13) | (ff << 26);
+        if (WALK) a.fwalk[i] = min(kfs[pass], maxn) | (ff << 26);
     }
 }
 

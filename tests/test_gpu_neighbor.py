@@ -11,10 +11,11 @@ import dpdsys as _sys
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["lane", "ballot"], autouse=True)
+@pytest.fixture(params=["range", "lane", "ballot"], autouse=True)
 def builder(request, monkeypatch):
-    """Both device builders -- k_build_lane (lane per row, the default) and
-    k_build (Alg. 3 warp ballot) -- must produce the reference rows."""
+    """All device builders -- k_build_range (culled range lists, the default),
+    k_build_lane (lane per row) and k_build (Alg. 3 warp ballot) -- must
+    produce the reference rows."""
     monkeypatch.setenv("DPDB_BUILDER", request.param)
     return request.param
 
@@ -154,12 +155,13 @@ def test_builders_give_identical_runs(monkeypatch):
     bit-identical trajectories: same pair sets, order-free fixed-point sums."""
     box, obox, st = _sys.fluid((12, 12, 12), 3.0, seed=17)
     out = {}
-    for b in ("lane", "ballot"):
+    for b in ("range", "lane", "ballot"):
         monkeypatch.setenv("DPDB_BUILDER", b)
         e = _sys.engine(box, st, run=dpd.RunConfig(rebuild_every=5))
         e.setup()
         e.step(17)
         out[b] = e.download()
-    for k in range(3):
-        assert np.array_equal(out["lane"].coord[k], out["ballot"].coord[k])
-        assert np.array_equal(out["lane"].force[k], out["ballot"].force[k])
+    for b in ("lane", "ballot"):
+        for k in range(3):
+            assert np.array_equal(out["range"].coord[k], out[b].coord[k])
+            assert np.array_equal(out["range"].force[k], out[b].force[k])
