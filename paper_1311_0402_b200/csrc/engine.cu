@@ -52,7 +52,7 @@ struct dpdb_ctx {
     uint8_t *sp{}, *sp2{};
     float4 *pos4{}, *vel4{};
     uint32_t *keys{}, *keys2{}, *vals{}, *vals2{}, *hist{};
-    uint32_t *cell_start{}, *rank_of_cell{}, *stencil{};
+    uint32_t *cell_start{}, *ostart{}, *rank_of_cell{}, *stencil{};
     uint8_t *stencil_n{}, *cell_flags{}, *stencil_code{};
     float4* cell_lo{};
     uint32_t *entries{}, *counts{}, *fwalk{};
@@ -307,6 +307,8 @@ int refresh_bond_index(dpdb_ctx* ctx) {
 int do_permute(dpdb_ctx* ctx, bool forces) {
     if (!ctx->n) {
         CK(cudaMemsetAsync(ctx->cell_start, 0, ((size_t)ctx->grid.n_total_cells + 1) * 4, ctx->stream));
+        if (ctx->ostart)
+            CK(cudaMemsetAsync(ctx->ostart, 0, ((size_t)ctx->grid.n_total_cells * 8 + 1) * 4, ctx->stream));
         ctx->have_sorted = true;
         return 0;
     }
@@ -329,6 +331,7 @@ int do_permute(dpdb_ctx* ctx, bool forces) {
     a.order = ctx->vals;
     a.keys = ctx->keys;
     a.cell_start = ctx->cell_start;
+    a.ostart = ctx->ostart;
     a.pos4 = ctx->pos4;
     a.vel4 = ctx->vel4;
     a.n = (uint32_t)ctx->n;
@@ -377,6 +380,7 @@ int do_build(dpdb_ctx* ctx, bool joined_out) {
     a.pos4 = ctx->pos4;
     a.keys = ctx->keys;
     a.cell_start = ctx->cell_start;
+    a.ostart = ctx->ostart;
     a.stencil = ctx->stencil;
     a.stencil_n = ctx->stencil_n;
     a.cell_flags = ctx->cell_flags;
@@ -728,6 +732,7 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         (rc = dalloc(ctx, ctx->hist, std::max<size_t>((size_t)256 * tiles + 256,
                                                       26 * (c / dpdb::MD_THREADS + 1) + 64))) ||
         (rc = dalloc(ctx, ctx->cell_start, (size_t)g.n_total_cells + 1)) ||
+        (g.sub_bits >= 1 && (rc = dalloc(ctx, ctx->ostart, (size_t)g.n_total_cells * 8 + 1))) ||
         (rc = dalloc(ctx, ctx->rank_of_cell, (size_t)g.n_total_cells)) ||
         (rc = dalloc(ctx, ctx->stencil, (size_t)g.n_local_cells * 32)) ||
         (rc = dalloc(ctx, ctx->stencil_n, (size_t)g.n_local_cells)) ||
@@ -788,7 +793,7 @@ int dpdb_destroy(dpdb_ctx* ctx) {
     md_release(ctx);
     void* ptrs[] = {ctx->tag, ctx->tag2, ctx->mol, ctx->mol2, ctx->sp, ctx->sp2, ctx->pos4,
                     ctx->vel4, ctx->keys, ctx->keys2, ctx->vals, ctx->vals2, ctx->hist,
-                    ctx->cell_start, ctx->rank_of_cell, ctx->stencil, ctx->stencil_n,
+                    ctx->cell_start, ctx->ostart, ctx->rank_of_cell, ctx->stencil, ctx->stencil_n,
                     ctx->cell_flags, ctx->stencil_code, ctx->cell_lo, ctx->entries, ctx->counts, ctx->fwalk, ctx->rowmeta,
                     ctx->err, ctx->red, ctx->red_out,
                     ctx->tmp_u32, ctx->bond_off, ctx->bond_partner, ctx->index_of_tag,

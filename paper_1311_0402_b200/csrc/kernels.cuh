@@ -359,6 +359,7 @@ struct PermuteArgs {
     const uint32_t* order;       // sorted vals: order[to] = from
     const uint32_t* keys;        // sorted keys
     uint32_t* cell_start;        // [n_total_cells + 1]
+    uint32_t* ostart;            // [8 n_total_cells + 1] octant starts (nullable, sub_bits >= 1)
     float4* pos4;
     float4* vel4;
     double centre[3];
@@ -401,6 +402,17 @@ __global__ void __launch_bounds__(256) k_permute(PermuteArgs a) {
     for (uint32_t c = c0; c <= r; ++c) a.cell_start[c] = t;
     if (t == a.n - 1)
         for (uint32_t c = r + 1; c <= a.n_total_cells; ++c) a.cell_start[c] = a.n;
+    if (a.ostart) {
+        // the same boundary detection one level down: octant = top 3 bits of
+        // the sub-cell Morton code, so a cell's particles come octant by octant
+        const int os = a.key_shift - 3;
+        const uint32_t omax = 8u * a.n_total_cells - 1u;
+        const uint32_t ro = min(a.keys[t] >> os, omax);
+        const uint32_t o0 = t == 0 ? 0u : min(a.keys[t - 1] >> os, omax) + 1u;
+        for (uint32_t c = o0; c <= ro; ++c) a.ostart[c] = t;
+        if (t == a.n - 1)
+            for (uint32_t c = ro + 1; c <= omax + 1u; ++c) a.ostart[c] = a.n;
+    }
 }
 
 // fp32 streams + signatures from the current fp64 state (no reorder)
@@ -431,6 +443,7 @@ struct BuildArgs {
     const float4* pos4;
     const uint32_t* keys;        // sorted keys (rank = key >> key_shift)
     const uint32_t* cell_start;
+    const uint32_t* ostart;      // k_build_range: octant starts [8 n_total_cells + 1] or null
     const uint32_t* stencil;     // [n_local_cells][32]
     const uint8_t* stencil_n;
     const uint8_t* cell_flags;
@@ -819,50 +832,73 @@ __global__ void __launch_bounds__(RB_THREADS, 4) k_build_range(BuildArgs a) {
             fl = a.cell_flags[r];
             pi = a.pos4[i];
         }
-        // ---- phase 1: ranges
-        float dm[3], dp[3];  // squared distance to the offset -1 / +1 slabs per axis
+        // ---- phase 1: ranges.  Per axis, the squared distance from pi to the
+        // lower / upper half of the cells at offset -1, 0, +1 (slab [lo, hi]:
+        // max(0, lo - l, l - hi)); an octant of a stencil cell is in reach iff
+        // the three axis terms sum to <= cut_cull.  The kept range of a cell is
+        // trimmed to [first kept octant, last kept octant]: particles are
+        // sorted octant by octant inside a cell, so this stays one range.
+        float hd[3][6];
         {
             const float4 lo = row ? a.cell_lo[r] : make_float4(0.f, 0.f, 0.f, 0.f);
             const float l[3] = {pi.x - lo.x, pi.y - lo.y, pi.z - lo.z};
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
-                const float m = fmaxf(l[k], 0.f), p = fmaxf(a.csz[k] - l[k], 0.f);
-                dm[k] = m * m;
-                dp[k] = p * p;
+                const float h = 0.5f * a.csz[k];
+#pragma unroll
+                for (int q = 0; q < 6; ++q) {
+                    const float s0 = (float)(q - 2) * h, s1 = s0 + h;  // slab [-a + q a/2, ...]
+                    const float d = fmaxf(fmaxf(s0 - l[k], l[k] - s1), 0.f);
+                    hd[k][q] = d * d;
+                }
             }
         }
         const uint32_t cut_lo = WALK ? b0 : i;  // excluded index range [cut_lo, i]
+        const uint32_t* otab = a.ostart ? a.ostart : a.cell_start;
+        const int osh = a.ostart ? 3 : 0;
         uint32_t nr = 0;
         const uint32_t* srow = a.stencil + (size_t)r * 32;
         const uint8_t* crow = a.stencil_code + (size_t)r * 32;
         bool big = false;
 #pragma unroll 1
         for (uint32_t s0 = 0; s0 < ns; s0 += 4) {
-            uint32_t sc[4], cd[4], st[4], en[4];
+            uint32_t sc[4], st[4], en[4], lo_i[4], hi_i[4];
+            bool kp[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const bool v = s0 + q < ns;
                 sc[q] = v ? srow[s0 + q] : 0u;
-                cd[q] = v ? crow[s0 + q] : 0u;
+                const uint32_t c = v ? crow[s0 + q] : 0u;
+                uint32_t m = 0xFFu;
+                if (c != 0xFFu) {
+                    float d0[3], d1[3];  // lower / upper half of the cell at this offset, per axis
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        const uint32_t o = (c >> (2 * k)) & 3u;
+                        d0[k] = o == 0u ? hd[k][0] : (o == 1u ? hd[k][2] : hd[k][4]);
+                        d1[k] = o == 0u ? hd[k][1] : (o == 1u ? hd[k][3] : hd[k][5]);
+                    }
+                    const float yz[4] = {d0[1] + d0[2], d1[1] + d0[2], d0[1] + d1[2], d1[1] + d1[2]};
+                    m = 0u;
+#pragma unroll
+                    for (int h = 0; h < 8; ++h)
+                        m |= (uint32_t)(((h & 1) ? d1[0] : d0[0]) + yz[h >> 1] <= a.cut_cull) << h;
+                }
+                if (!a.ostart) m = m ? 1u : 0u;  // cell granularity only
+                kp[q] = v && m != 0u;
+                lo_i[q] = (sc[q] << osh) + (m ? __ffs(m) - 1 : 0);
+                hi_i[q] = (sc[q] << osh) + (m ? 32 - __clz(m) : 1);
             }
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                st[q] = a.cell_start[sc[q]];
-                en[q] = a.cell_start[sc[q] + 1];
+                st[q] = otab[lo_i[q]];
+                en[q] = otab[hi_i[q]];
             }
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 // branch-free: both pieces are always written, nr advances only
                 // over the kept non-empty ones (slot RB_SLOTS - 1 absorbs the rest)
-                const uint32_t c = cd[q];
-                float d2 = 0.f;
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    const uint32_t o = (c >> (2 * k)) & 3u;
-                    const float v = (o & 2u) ? dp[k] : dm[k];
-                    d2 += (o & 1u) ? 0.f : v;
-                }
-                const bool keep = s0 + q < ns && (c == 0xFFu || d2 <= a.cut_cull);
+                const bool keep = kp[q];
                 const uint32_t e1 = min(en[q], cut_lo), s2 = max(st[q], i + 1u);
                 const uint32_t l1 = e1 > st[q] ? e1 - st[q] : 0u;
                 const uint32_t l2 = en[q] > s2 ? en[q] - s2 : 0u;
