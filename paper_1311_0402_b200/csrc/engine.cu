@@ -50,7 +50,7 @@ struct dpdb_ctx {
     float *f[3]{}, *f2[3]{};
     uint32_t *tag{}, *tag2{}, *mol{}, *mol2{};
     uint8_t *sp{}, *sp2{};
-    float4 *pos4{}, *vel4{};
+    float4 *pos4{}, *vel4{}, *pos4n{}, *vel4n{};  // n: next-step streams of the fused force pass
     uint32_t *keys{}, *keys2{}, *vals{}, *vals2{}, *hist{};
     uint32_t *cell_start{}, *ostart{}, *rank_of_cell{}, *stencil{};
     uint8_t *stencil_n{}, *cell_flags{}, *stencil_code{};
@@ -74,6 +74,7 @@ struct dpdb_ctx {
     // flags
     bool has_mol = false, have_sorted = false, have_table = false, tiled = true, joined = false;
     bool multi = false;  // n_species > 1: species packed into pos4.w bits 28-31
+    bool no_fuse = false;  // DPDB_FUSE=0: keep the Verlet pass a separate kernel (A/B)
     int64_t step = 0;
     std::string last_error;
     // stage timing
@@ -232,9 +233,7 @@ void wrap_lengths(const dpdb_ctx* ctx, float L[3], float H[3]) {
 // across bricks -- a local that crosses the seam keeps its unwrapped
 // coordinate (consistent with its neighbors and with the shifted ghost
 // copies) until the next rebuild wraps and migrates it
-template <bool P2, bool P1, bool KEYS, bool STREAMS>
-int launch_integrate(dpdb_ctx* ctx, bool defer_wrap = false) {
-    if (!ctx->n) return 0;
+dpdb::IntegrateArgs integrate_args(dpdb_ctx* ctx, bool defer_wrap) {
     dpdb::IntegrateArgs a{};
     for (int k = 0; k < 3; ++k) {
         a.x[k] = ctx->x[k];
@@ -256,6 +255,13 @@ int launch_integrate(dpdb_ctx* ctx, bool defer_wrap = false) {
     a.dt = ctx->params.dt;
     a.h = 0.5 * ctx->params.dt;
     a.n = (uint32_t)ctx->n;
+    return a;
+}
+
+template <bool P2, bool P1, bool KEYS, bool STREAMS>
+int launch_integrate(dpdb_ctx* ctx, bool defer_wrap = false) {
+    if (!ctx->n) return 0;
+    const dpdb::IntegrateArgs a = integrate_args(ctx, defer_wrap);
     dpdb::k_integrate<P2, P1, KEYS, STREAMS><<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(a);
     CKL();
     ctx->launches[ST_INTEGRATE]++;
@@ -458,20 +464,24 @@ void force_launch(dpdb_ctx* ctx, const dpdb::ForceArgs& a, bool body) {
 }
 
 template <bool MULTI, bool BODY>
-void force_walk_launch(dpdb_ctx* ctx, const dpdb::ForceArgs& a) {
+void force_walk_launch(dpdb_ctx* ctx, const dpdb::ForceArgs& a, int fuse) {
     const unsigned nb = blocks_for(ctx->n, dpdb::FORCE_BLOCK);
     constexpr int T = dpdb::FORCE_WARPS * 32;
-    if (ctx->maxn == 128)
-        dpdb::k_force_walk<MULTI, BODY, 128><<<nb, T, 0, ctx->stream>>>(a);
+    if (fuse == dpdb::FUSE_STREAMS)  // fused variants: maxn == 128 only (can_fuse)
+        dpdb::k_force_walk<MULTI, BODY, 128, dpdb::FUSE_STREAMS><<<nb, T, 0, ctx->stream>>>(a);
+    else if (fuse == dpdb::FUSE_KEYS)
+        dpdb::k_force_walk<MULTI, BODY, 128, dpdb::FUSE_KEYS><<<nb, T, 0, ctx->stream>>>(a);
+    else if (ctx->maxn == 128)
+        dpdb::k_force_walk<MULTI, BODY, 128, dpdb::FUSE_NONE><<<nb, T, 0, ctx->stream>>>(a);
     else
-        dpdb::k_force_walk<MULTI, BODY, 0><<<nb, T, 0, ctx->stream>>>(a);
+        dpdb::k_force_walk<MULTI, BODY, 0, dpdb::FUSE_NONE><<<nb, T, 0, ctx->stream>>>(a);
 }
 
 template <bool MULTI>
-void force_dispatch_layout(dpdb_ctx* ctx, const dpdb::ForceArgs& a, bool body) {
+void force_dispatch_layout(dpdb_ctx* ctx, const dpdb::ForceArgs& a, bool body, int fuse) {
     if (ctx->walk) {
-        if (body) force_walk_launch<MULTI, true>(ctx, a);
-        else force_walk_launch<MULTI, false>(ctx, a);
+        if (body) force_walk_launch<MULTI, true>(ctx, a, fuse);
+        else force_walk_launch<MULTI, false>(ctx, a, fuse);
     }
     else if (ctx->tiled && !ctx->joined) force_launch<MULTI, true, false>(ctx, a, body);
     else if (ctx->tiled) force_launch<MULTI, true, true>(ctx, a, body);
@@ -479,7 +489,18 @@ void force_dispatch_layout(dpdb_ctx* ctx, const dpdb::ForceArgs& a, bool body) {
     else force_launch<MULTI, false, true>(ctx, a, body);
 }
 
-int do_forces(dpdb_ctx* ctx, uint32_t step) {
+// Whether the step loop may run the next Verlet pass inside the force kernel:
+// single domain, walk layout with 128-slot rows, no bonds (their forces are
+// added by a separate pass after the pair forces).
+bool can_fuse(const dpdb_ctx* ctx) {
+    return ctx->walk && ctx->maxn == 128 && !ctx->n_bonds && !ctx->md_valid &&
+           ctx->dims[0] * ctx->dims[1] * ctx->dims[2] == 1 && !ctx->no_fuse;
+}
+
+// fuse (step loop only, can_fuse): FUSE_STREAMS / FUSE_KEYS run phase 2 of
+// this step + phase 1 of the next in the force kernel's epilogue; the forces
+// themselves are then not stored.
+int do_forces(dpdb_ctx* ctx, uint32_t step, int fuse = dpdb::FUSE_NONE) {
     if (!ctx->have_table) return fail(ctx, DPDB_ECONFIG, "compute_forces: neighbor table not built");
     if (!ctx->n) return 0;
     const dpdb_params& p = ctx->params;
@@ -515,10 +536,15 @@ int do_forces(dpdb_ctx* ctx, uint32_t step) {
         a.tg[q] = (float)p.gamma[q];
         a.ts[q] = (float)(ctx->sigma[q] / std::sqrt(p.dt));
     }
+    if (fuse != dpdb::FUSE_NONE) {
+        a.ia = integrate_args(ctx, false);
+        a.pos4n = ctx->pos4n;
+        a.vel4n = ctx->vel4n;
+    }
     if (ctx->multi || a.smode != 1)
-        force_dispatch_layout<true>(ctx, a, body);
+        force_dispatch_layout<true>(ctx, a, body, fuse);
     else
-        force_dispatch_layout<false>(ctx, a, body);
+        force_dispatch_layout<false>(ctx, a, body, fuse);
     CKL();
     ctx->launches[ST_FORCE]++;
     if (ctx->n_bonds) {
@@ -661,6 +687,7 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
     if (const char* b = std::getenv("DPDB_BUILDER"))
         ctx->builder = !std::strcmp(b, "ballot") ? 0 : !std::strcmp(b, "lane") ? 1 : 2;
     ctx->multi = params->n_species > 1;
+    if (const char* f = std::getenv("DPDB_FUSE")) ctx->no_fuse = std::strcmp(f, "0") == 0;
     for (int q = 0; q < ns * ns; ++q) ctx->sigma[q] = std::sqrt(2.0 * params->gamma[q] * params->kbt);
     std::string err;
     // brick geometry (decompose): uniform half-open slabs
@@ -727,6 +754,7 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         (rc = dalloc(ctx, ctx->sp, c)) || (rc = dalloc(ctx, ctx->sp2, c)) ||
         (rc = dalloc(ctx, ctx->mol, c)) || (rc = dalloc(ctx, ctx->mol2, c)) ||
         (rc = dalloc(ctx, ctx->pos4, c)) || (rc = dalloc(ctx, ctx->vel4, c)) ||
+        (rc = dalloc(ctx, ctx->pos4n, c)) || (rc = dalloc(ctx, ctx->vel4n, c)) ||
         (rc = dalloc(ctx, ctx->keys, c)) || (rc = dalloc(ctx, ctx->keys2, c)) ||
         (rc = dalloc(ctx, ctx->vals, c)) || (rc = dalloc(ctx, ctx->vals2, c)) ||
         (rc = dalloc(ctx, ctx->hist, std::max<size_t>((size_t)256 * tiles + 256,
@@ -792,15 +820,15 @@ int dpdb_destroy(dpdb_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     md_release(ctx);
     void* ptrs[] = {ctx->tag, ctx->tag2, ctx->mol, ctx->mol2, ctx->sp, ctx->sp2, ctx->pos4,
-                    ctx->vel4, ctx->keys, ctx->keys2, ctx->vals, ctx->vals2, ctx->hist,
+                    ctx->vel4, ctx->pos4n, ctx->vel4n, ctx->keys, ctx->keys2, ctx->vals, ctx->vals2, ctx->hist,
                     ctx->cell_start, ctx->ostart, ctx->rank_of_cell, ctx->stencil, ctx->stencil_n,
                     ctx->cell_flags, ctx->stencil_code, ctx->cell_lo, ctx->entries, ctx->counts, ctx->fwalk, ctx->rowmeta,
                     ctx->err, ctx->red, ctx->red_out,
                     ctx->tmp_u32, ctx->bond_off, ctx->bond_partner, ctx->index_of_tag,
                     ctx->bond_k, ctx->bond_r0, ctx->md_masks, ctx->md_mig, ctx->md_slot,
                     ctx->md_doff, ctx->md_dbase, ctx->md_mlist, ctx->md_glist};
-    for (void* p : ptrs)
-        if (p) cudaFree(p);
+    for (size_t q = 0; q < sizeof(ptrs) / sizeof(ptrs[0]); ++q)  // each buffer once
+        if (ptrs[q] && std::find(ptrs, ptrs + q, ptrs[q]) == ptrs + q) cudaFree(ptrs[q]);
     for (int k = 0; k < 3; ++k) {
         void* q[] = {ctx->x[k], ctx->v[k], ctx->x2[k], ctx->v2[k], ctx->f[k], ctx->f2[k]};
         for (void* p : q)
@@ -1235,27 +1263,42 @@ int dpdb_setup(dpdb_ctx* ctx) {
 }
 
 namespace {
+// Alg. 1 loop.  When can_fuse, the Verlet pass between two force
+// evaluations (phase 2 of step n + phase 1 of step n+1, plus the next step's
+// fp32 streams or sort keys) runs in the epilogue of step n's force kernel,
+// on the forces the block just reduced -- same arithmetic, one HBM pass fewer.
 int run_steps(dpdb_ctx* ctx, int64_t nsteps) {
     if (!ctx->have_table) return fail(ctx, DPDB_ECONFIG, "step: call dpdb_setup first");
+    bool integrated = false;  // this step's Verlet pass already ran in the last force kernel
     for (int64_t s = 0; s < nsteps; ++s) {
         ctx->step += 1;
         const bool rebuild = ctx->step % ctx->run.rebuild_every == 0;
         mark(ctx, ST_OTHER);
         if (rebuild) {
-            if (s > 0) TRY((launch_integrate<true, true, true, false>(ctx)));
-            else TRY((launch_integrate<false, true, true, false>(ctx)));
-            mark(ctx, ST_INTEGRATE);
+            if (!integrated) {
+                if (s > 0) TRY((launch_integrate<true, true, true, false>(ctx)));
+                else TRY((launch_integrate<false, true, true, false>(ctx)));
+                mark(ctx, ST_INTEGRATE);
+            }
             TRY(do_sort(ctx));
             TRY(do_permute(ctx, false));
             mark(ctx, ST_SORT);
             TRY(do_build(ctx, true));
             mark(ctx, ST_BUILD);
-        } else {
+        } else if (!integrated) {
             if (s > 0) TRY((launch_integrate<true, true, false, true>(ctx)));
             else TRY((launch_integrate<false, true, false, true>(ctx)));
             mark(ctx, ST_INTEGRATE);
         }
-        TRY(do_forces(ctx, (uint32_t)ctx->step));
+        const bool fuse = s + 1 < nsteps && can_fuse(ctx);
+        const bool next_rebuild = (ctx->step + 1) % ctx->run.rebuild_every == 0;
+        TRY(do_forces(ctx, (uint32_t)ctx->step,
+                      fuse ? (next_rebuild ? dpdb::FUSE_KEYS : dpdb::FUSE_STREAMS) : dpdb::FUSE_NONE));
+        if (fuse && !next_rebuild) {
+            std::swap(ctx->pos4, ctx->pos4n);
+            std::swap(ctx->vel4, ctx->vel4n);
+        }
+        integrated = fuse;
         mark(ctx, ST_FORCE);
     }
     if (nsteps > 0) {

@@ -28,7 +28,16 @@ struct ForceArgs {
     int smode;                     // 1, 2, 3: integer weight exponent; 0: fastpow path
     uint32_t ns;                   // species count (MULTI)
     float ta[16], tg[16], ts[16];  // a_ij, gamma_ij, sigma_ij / sqrt(dt)
+    // k_force_walk<.., FUSE>: the next Verlet pass (phase 2 of this step +
+    // phase 1 of the next) runs in the epilogue on the block's fresh forces;
+    // streams go to pos4n / vel4n (the other buffer: neighbors still read this
+    // step's), keys to ia.keys / ia.vals when the next step rebuilds.
+    IntegrateArgs ia;
+    float4* pos4n;
+    float4* vel4n;
 };
+
+enum ForceFuse : int { FUSE_NONE = 0, FUSE_STREAMS = 1, FUSE_KEYS = 2 };
 
 // approximate fp32 transcendentals with flush-to-zero (the pair path only;
 // the bit-exact builder/integrator paths never use these)
@@ -72,6 +81,8 @@ __device__ __forceinline__ float gaussian_hot(uint32_t ua, uint32_t ub) {
     const float s = sin_ftz(3.14159265358979f * y);
     return (ub >> 31) ? rad * s : -(rad * s);
 }
+
+__device__ __forceinline__ float gaussian_pair(uint32_t ua, uint32_t ub) { return gaussian_hot(ua, ub); }
 
 // Branch-free fp32 minimum image for the walk force kernel: L = 0 (and
 // invL = 0) on axes without wrap.  d - L*rint(d/L) equals min_image_f's
@@ -200,7 +211,7 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(ForceArgs a) {
                 uint32_t u0 = ifirst ? sig_i : sig_j;
                 uint32_t u1 = (ifirst ? sig_j : sig_i) ^ a.step_mix;
                 tea4(u0, u1);
-                const float xi = gaussian_hot(u0, u1);
+                const float xi = gaussian_pair(u0, u1);
                 const float r2 = fmaf(d.x, d.x, fmaf(d.y, d.y, d.z * d.z));
                 const float rinv = rsqrt_ftz(r2);
                 const float w = fmaxf(fmaf(-r2 * rinv, a.inv_rc, 1.f), 0.f);
@@ -321,9 +332,13 @@ constexpr bool FW_UNCOND = DPDB_FW_UNCOND;
 #ifndef FW_MINB
 #define FW_MINB 4  // resident CTAs per SM the register allocation must allow (A/B: 1, 3, 4 -> 4 best)
 #endif  // A/B switch: unpredicated phase-A loads
+#ifndef DPDB_FW_PREFETCH
+#define DPDB_FW_PREFETCH 0
+#endif
+constexpr bool FW_PREFETCH = DPDB_FW_PREFETCH;  // A/B switch: L1 prefetch of vel4[j] in phase A
 constexpr int FW_Q = 160;  // < 32 leftovers + 4 x 32 hits per group
 
-template <bool GENERAL, bool BODY, int MAXN>
+template <bool GENERAL, bool BODY, int MAXN, int FUSE>
 __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceArgs a) {
     static_assert(FORCE_TILES == 2 * FORCE_WARPS, "tile pairing assumes 2 tiles per warp");
     __shared__ uint32_t q_j[FORCE_WARPS][FW_Q];  // j | owner lane << 27
@@ -395,7 +410,7 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceA
                 uint32_t u0 = ifirst ? sig_i : sig_j;
                 uint32_t u1 = (ifirst ? sig_j : sig_i) ^ a.step_mix;
                 tea4(u0, u1);
-                const float xi = gaussian_hot(u0, u1);
+                const float xi = gaussian_pair(u0, u1);
                 const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
                 if (r2 == 0.f) {
                     coincident = true;
@@ -434,6 +449,7 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceA
         // arithmetic, which drops the walk layout's skin tag (bit 31).
         const uint32_t* ep = a.entries + (size_t)(b0 + il0) * maxn + lane;
         const char* pb = reinterpret_cast<const char*>(a.pos4);
+        const char* vb = reinterpret_cast<const char*>(a.vel4);
         uint32_t* qw = q_j[warp];
         auto phase_a = [&](auto wrap_c) {
             constexpr bool WRAP = decltype(wrap_c)::value;
@@ -471,6 +487,8 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceA
                     const bool hit = m0 + k < tot && r2 <= rc2;
                     const uint32_t bal = __ballot_sync(0xFFFFFFFFu, hit);
                     if (hit) qw[qtail + __popc(bal & lt)] = (cur[k] & 0x7FFFFFFFu) | lanebits;
+                    if (FW_PREFETCH && hit)  // phase B's vel4[j] gather then hits L1
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(vb + ((size_t)(cur[k] & 0x7FFFFFFFu) << 4)));
                     qtail += __popc(bal);
                 }
                 // drain whole batches, then move the (< 32) leftovers to the front
@@ -509,8 +527,32 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceA
         __syncwarp();
     }
     if (coincident) raise_err(a.err, DPDB_EPHYSICS, EW_COINCIDENT, bad_tag, 0u);
+    // FUSE: fetch the block's fp64 x, v and tags for the Verlet epilogue before
+    // the barrier, so the loads overlap the wait for the block's last warps
+    constexpr int PER_T = FORCE_BLOCK / (FORCE_WARPS * 32);
+    double ex[FUSE ? PER_T : 1][6];
+    uint32_t etag[FUSE ? PER_T : 1], esp[FUSE ? PER_T : 1];
+    if (FUSE != FUSE_NONE) {
+#pragma unroll
+        for (int q = 0; q < PER_T; ++q) {
+            const uint32_t t = threadIdx.x + q * FORCE_WARPS * 32;
+            if (t < bn) {
+                const uint32_t i = b0 + t;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    ex[q][k] = a.ia.x[k][i];
+                    ex[q][3 + k] = a.ia.v[k][i];
+                }
+                etag[q] = a.ia.tag[i];
+                esp[q] = a.ia.sp ? a.ia.sp[i] : 0u;
+            }
+        }
+    }
     __syncthreads();
-    for (uint32_t t = threadIdx.x; t < bn; t += FORCE_WARPS * 32) {
+#pragma unroll
+    for (int q = 0; q < PER_T; ++q) {
+        const uint32_t t = threadIdx.x + q * FORCE_WARPS * 32;
+        if (t >= bn) break;
         const uint32_t i = b0 + t;
         float fx = (float)acc[3 * t + 0] * FIX_INV;
         float fy = (float)acc[3 * t + 1] * FIX_INV;
@@ -524,8 +566,17 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceA
             else
                 fz += g;
         }
-        a.f[0][i] = fx;
-        a.f[1][i] = fy;
-        a.f[2][i] = fz;
+        if (FUSE == FUSE_NONE) {
+            a.f[0][i] = fx;
+            a.f[1][i] = fy;
+            a.f[2][i] = fz;
+        } else {
+            const float f[3] = {fx, fy, fz};
+            const int qq = FUSE ? q : 0;
+            const double x[3] = {ex[qq][0], ex[qq][1], ex[qq][2]};
+            const double v[3] = {ex[qq][3], ex[qq][4], ex[qq][5]};
+            integrate_particle<true, true, FUSE == FUSE_KEYS, FUSE == FUSE_STREAMS>(
+                a.ia, i, f, x, v, etag[qq], esp[qq], a.pos4n, a.vel4n);
+        }
     }
 }

@@ -147,21 +147,24 @@ struct IntegrateArgs {
 // writes the fp32 streams) or the fp32 force streams with signatures.
 // Each half kick is its own rounding so the fp64 trajectory equals the
 // reference's phase2-then-phase1 sequence bit for bit.
+// One particle; f is the particle's force (k_integrate reads it from memory,
+// the fused pair-force kernel hands over its freshly reduced sum).
 template <bool PHASE2, bool PHASE1, bool KEYS, bool STREAMS>
-__global__ void __launch_bounds__(256) k_integrate(IntegrateArgs a) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= a.n) return;
+__device__ __forceinline__ void integrate_particle(const IntegrateArgs& a, uint32_t i, const float f[3],
+                                                   const double xin[3], const double vin[3],
+                                                   uint32_t tag, uint32_t spc, float4* pos4,
+                                                   float4* vel4) {
     double xs[3], vs[3];
     bool ok = true;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        double v = a.v[k][i];
+        double v = vin[k];
         if (PHASE2 || PHASE1) {
-            const double f = (double)a.f[k][i];
-            if (PHASE2) v = __dadd_rn(v, __dmul_rn(a.h, f));
-            if (PHASE1) v = __dadd_rn(v, __dmul_rn(a.h, f));
+            const double fk = (double)f[k];
+            if (PHASE2) v = __dadd_rn(v, __dmul_rn(a.h, fk));
+            if (PHASE1) v = __dadd_rn(v, __dmul_rn(a.h, fk));
         }
-        double x = a.x[k][i];
+        double x = xin[k];
         if (PHASE1) {
             x = __dadd_rn(x, __dmul_rn(a.dt, v));
             if (!(isfinite(x) && isfinite(v)))
@@ -174,22 +177,38 @@ __global__ void __launch_bounds__(256) k_integrate(IntegrateArgs a) {
         xs[k] = x;
         vs[k] = v;
     }
-    const uint32_t tag = (STREAMS || !ok) ? a.tag[i] : 0u;
     if (!ok) raise_err(a.err, DPDB_EPHYSICS, EW_NONFINITE, tag, 0);
     if (KEYS) {
         uint32_t key = 0xFFFFFFFFu;
         if (!sort_key_of(a.grid, xs[0], xs[1], xs[2], key))
-            raise_err(a.err, DPDB_EPROTOCOL, EW_MIGRATION, a.tag[i], 0);
+            raise_err(a.err, DPDB_EPROTOCOL, EW_MIGRATION, tag, 0);
         a.keys[i] = key;
         a.vals[i] = i;
     }
     if (STREAMS) {
         const uint32_t sig = make_signature(tag, vs[0], vs[1], vs[2]);
-        const uint32_t tw = a.sp ? (tag | ((uint32_t)a.sp[i] << 28)) : tag;  // species in bits 28+
-        a.pos4[i] = make_float4((float)(xs[0] - a.grid.centre[0]), (float)(xs[1] - a.grid.centre[1]),
-                                (float)(xs[2] - a.grid.centre[2]), __uint_as_float(tw));
-        a.vel4[i] = make_float4((float)vs[0], (float)vs[1], (float)vs[2], __uint_as_float(sig));
+        const uint32_t tw = a.sp ? (tag | (spc << 28)) : tag;  // species in bits 28+
+        pos4[i] = make_float4((float)(xs[0] - a.grid.centre[0]), (float)(xs[1] - a.grid.centre[1]),
+                              (float)(xs[2] - a.grid.centre[2]), __uint_as_float(tw));
+        vel4[i] = make_float4((float)vs[0], (float)vs[1], (float)vs[2], __uint_as_float(sig));
     }
+}
+
+template <bool PHASE2, bool PHASE1, bool KEYS, bool STREAMS>
+__global__ void __launch_bounds__(256) k_integrate(IntegrateArgs a) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    float f[3] = {0.f, 0.f, 0.f};
+    double x[3], v[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        if (PHASE2 || PHASE1) f[k] = a.f[k][i];
+        x[k] = a.x[k][i];
+        v[k] = a.v[k][i];
+    }
+    const uint32_t tag = (STREAMS || PHASE1) ? a.tag[i] : 0u;  // signature / error report
+    const uint32_t spc = (STREAMS && a.sp) ? a.sp[i] : 0u;
+    integrate_particle<PHASE2, PHASE1, KEYS, STREAMS>(a, i, f, x, v, tag, spc, a.pos4, a.vel4);
 }
 
 // ------------------------------------------------------- radix sort
@@ -796,6 +815,15 @@ __global__ void __launch_bounds__(256) k_build_lane(BuildArgs a) {
 //        transposes of the block's front entries (unwalk restores them) --
 //        but they are counted (shared-memory integer adds, order-free) so
 //        counts and the overflow check equal the reference's full rows.
+// predicated select (keeps the compiler from branching on small selects)
+__device__ __forceinline__ float fsel(bool p, float a, float b) {
+    float r;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\tselp.f32 %0, %1, %2, q;\n\t}"
+        : "=f"(r)
+        : "f"(a), "f"(b), "r"((uint32_t)p));
+    return r;
+}
+
 constexpr int RB_BLOCK = 512;    // == FORCE_BLOCK (force.cuh)
 constexpr int RB_THREADS = 256;
 constexpr int RB_SLOTS = 29;     // 27 stencil cells + one split by the cut-out + a trash slot
@@ -862,21 +890,24 @@ __global__ void __launch_bounds__(RB_THREADS, 4) k_build_range(BuildArgs a) {
         bool big = false;
 #pragma unroll 1
         for (uint32_t s0 = 0; s0 < ns; s0 += 4) {
-            uint32_t sc[4], st[4], en[4], lo_i[4], hi_i[4];
+            uint32_t st[4], en[4], lo_i[4], hi_i[4];
             bool kp[4];
+            // four stencil slots per 16-byte load (rows are padded to 32)
+            const uint4 sc4 = *reinterpret_cast<const uint4*>(srow + s0);
+            const uint32_t cd4 = *reinterpret_cast<const uint32_t*>(crow + s0);
+            const uint32_t sc[4] = {sc4.x, sc4.y, sc4.z, sc4.w};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const bool v = s0 + q < ns;
-                sc[q] = v ? srow[s0 + q] : 0u;
-                const uint32_t c = v ? crow[s0 + q] : 0u;
+                const uint32_t c = (cd4 >> (8 * q)) & 0xFFu;
                 uint32_t m = 0xFFu;
                 if (c != 0xFFu) {
                     float d0[3], d1[3];  // lower / upper half of the cell at this offset, per axis
 #pragma unroll
                     for (int k = 0; k < 3; ++k) {
                         const uint32_t o = (c >> (2 * k)) & 3u;
-                        d0[k] = o == 0u ? hd[k][0] : (o == 1u ? hd[k][2] : hd[k][4]);
-                        d1[k] = o == 0u ? hd[k][1] : (o == 1u ? hd[k][3] : hd[k][5]);
+                        d0[k] = fsel(o == 2u, hd[k][4], fsel(o == 0u, hd[k][0], hd[k][2]));
+                        d1[k] = fsel(o == 2u, hd[k][5], fsel(o == 0u, hd[k][1], hd[k][3]));
                     }
                     const float yz[4] = {d0[1] + d0[2], d1[1] + d0[2], d0[1] + d1[2], d1[1] + d1[2]};
                     m = 0u;
@@ -1191,7 +1222,7 @@ __global__ void k_eval(int op, uint32_t n, const void* in0, const void* in1, uin
             static_cast<float*>(out)[i] = fastlog32(u0[i]);
             break;
         case DPDB_OP_GAUSSIAN_HOT:
-            static_cast<float*>(out)[i] = gaussian_hot(u0[i], u1[i]);
+            static_cast<float*>(out)[i] = gaussian_pair(u0[i], u1[i]);
             break;
         case DPDB_OP_STEP_MIX:
             static_cast<uint32_t*>(out)[i] = step_mix_of(u0[i], u1[i]);

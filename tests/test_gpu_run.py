@@ -79,6 +79,36 @@ def test_fused_step_equals_stagewise_api():
         assert np.array_equal(u, w)
 
 
+@pytest.mark.parametrize("case", ["poiseuille_walls", "two_species"])
+def test_fused_force_integrate_equals_separate_pass(monkeypatch, case):
+    """The step loop runs the Verlet pass inside the force kernel's epilogue
+    (DPDB_FUSE default); DPDB_FUSE=0 keeps it a separate kernel.  Both give
+    the same trajectory bit for bit, across rebuilds (the fused pass then
+    writes the sort keys), with body force + walls and with two species."""
+    if case == "poiseuille_walls":
+        box, obox, st = _sys.fluid((10, 8, 12), 3.0, (1, 1, 0), seed=23, wall=(0, 0, 1))
+        params, run = dpd.PairParams(), dpd.RunConfig(rebuild_every=4, body_force=0.05, drive_axis=0,
+                                                      partition_axis=2)
+    else:
+        box, obox, st = _sys.fluid((11, 11, 11), 3.0, seed=29)
+        st = list(st)
+        sp = (np.arange(len(st[0])) % 2).astype(np.uint8)
+        params, run = dpd.PairParams.make(2, [25, 40, 40, 25], 4.5, 1.0, 1.0, 1.0, 0.01), dpd.RunConfig(rebuild_every=5)
+    out = []
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("DPDB_FUSE", fuse)
+        e = dpd.Engine(box, params, run, capacity=len(st[0]))
+        ps = dpd.ParticleStore.from_arrays(*st)
+        if case == "two_species":
+            ps.species = sp
+        e.upload(ps)
+        e.setup()
+        e.step(13)
+        out.append(e.download())
+    for u, w in zip(out[0].coord + out[0].veloc + out[0].force, out[1].coord + out[1].veloc + out[1].force):
+        assert np.array_equal(u, w)
+
+
 def test_first_step_vs_oracle_driver():
     """Setup + one step against the oracle's Alg. 1 driver.  After one step
     the fp64 positions agree to fp32-force rounding; beyond that trajectories
