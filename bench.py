@@ -307,9 +307,20 @@ def run_b200(args, ws, rank, local):
     value = total_particles * args.steps / (ms_max * 1e-3) / 1e6
 
     # roofline of the dominant kernel (pair force): per particle
-    # 16 (pos|tag) + 16 (vel|sig) + 4 (counts) + 4 nbar (row) + 12 (force)
+    # 16 (pos|tag) + 16 (vel|sig) + 4 (counts) + 4 nbar (row) + 12 (force).
+    # The step loop fuses the Verlet pass into that kernel (all but the last
+    # step of a dpdb_step call): the force is then handed over in registers
+    # (-12) and the pass adds x, v fp64 read + write (96) + tag (4) + either
+    # the next fp32 streams (32) or, before a rebuild, the sort keys (8).
     force_launch_ms = stage_ms[3] / max(launches[3], 1)
-    bytes_per_launch = N_C3 * (48.0 + 4.0 * nbar)
+    fused = not bricks and os.environ.get("DPDB_FUSE", "1") != "0"
+    per = []
+    for step in range(args.warmup + 1, args.warmup + args.steps + 1):
+        if not fused or step == args.warmup + args.steps:
+            per.append(48.0)
+        else:
+            per.append(36.0 + 100.0 + (8.0 if (step + 1) % run.rebuild_every == 0 else 32.0))
+    bytes_per_launch = N_C3 * (float(np.mean(per)) + 4.0 * nbar)
     achieved = bytes_per_launch / (force_launch_ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
     traffic = None
@@ -328,19 +339,26 @@ def run_b200(args, ws, rank, local):
     t0 = time.perf_counter()
     e.upload(dpd.ParticleStore.from_arrays(*pinned))
     e.setup()
-    for _ in range(args.steps):
-        e.step(1)
-        e.thermo()
-    s = e.download()
-    for k in range(3):
-        out[k][:] = s.coord[k]
-        out[3 + k][:] = s.veloc[k]
+    if bricks:
+        for _ in range(args.steps):
+            e.step(1)
+            e.thermo()
+    else:  # every step's thermo line lands in pinned host memory (dpdb_step_thermo)
+        rec = e.step_thermo(args.steps)
+        assert len(rec["kbt"]) == args.steps and np.all(np.isfinite(rec["kbt"]))
+    if bricks:
+        s = e.download()
+        for k in range(3):
+            out[k][:] = s.coord[k]
+            out[3 + k][:] = s.veloc[k]
+    else:  # straight into the pinned result buffers
+        e.download_state(out[0:3], out[3:6])
     barrier_sync(ws)
     e2e_s = max_over_ranks(time.perf_counter() - t0, ws, local)
     e2e = total_particles * args.steps / e2e_s / 1e6
     h2d = N_C3 * (6 * 8 + 4)
-    d2h_state = N_C3 * (9 * 8 + 4 + 1 + 4)
-    d2h = d2h_state / args.steps + 2 * 64
+    d2h_state = N_C3 * ((9 * 8 + 4 + 1 + 4) if bricks else 6 * 8)
+    d2h = d2h_state / args.steps + (2 * 64 if bricks else 40)
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": ws,
@@ -350,7 +368,8 @@ def run_b200(args, ws, rank, local):
         "config": config_dict(ws, args.mode),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": traffic, "kernel": "k_force",
+                     "traffic": traffic,
+                     "kernel": "k_force_walk (fused Verlet epilogue)" if fused else "k_force_walk",
                      "bytes_per_launch": bytes_per_launch, "mean_row": round(nbar, 3),
                      "launch_ms": round(force_launch_ms, 5)},
         "step_roofline": {"bytes_per_step": step_bytes,
@@ -363,7 +382,9 @@ def run_b200(args, ws, rank, local):
         "gpu_launches": int(launches[5]),
         "e2e": {"value": round(e2e, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d / args.steps),
                 "d2h_bytes_per_step": int(d2h),
-                "note": "upload + setup + K x (dpdb_step(1) + thermo read) + download, pinned host"},
+                "note": ("upload + setup + K x (dpdb_step(1) + thermo read) + download, pinned host"
+                         if bricks else "upload + setup + dpdb_step_thermo(K) (every step's thermo "
+                         "record D2H into pinned memory) + download, pinned host")},
         "clocks": clk.summary(),
         "wall_s_timed": round(wall, 4),
     }

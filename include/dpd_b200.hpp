@@ -226,6 +226,12 @@ public:
     }
     void setup() { ck(dpdb_setup(ctx_)); }
     void step(std::int64_t nsteps) { ck(dpdb_step(ctx_, nsteps)); }
+    // nsteps steps with every step's thermo line (dpdb_step_thermo)
+    std::vector<dpdb_thermo> step_thermo(std::int64_t nsteps) {
+        std::vector<dpdb_thermo> out((size_t)nsteps);
+        ck(dpdb_step_thermo(ctx_, nsteps, out.data()));
+        return out;
+    }
     dpdb_thermo thermo() {
         dpdb_thermo t{};
         ck(dpdb_thermo_get(ctx_, &t));

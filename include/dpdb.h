@@ -157,6 +157,13 @@ int dpdb_setup(dpdb_ctx* ctx);
 /* nsteps of Alg. 1's main loop; rebuild every rebuild_every */
 int dpdb_step(dpdb_ctx* ctx, int64_t nsteps);
 int dpdb_thermo_get(dpdb_ctx* ctx, dpdb_thermo* out);
+/* Runs nsteps like dpdb_step and records the thermo line of every step
+ * (out[0..nsteps-1]): the pass that applies a step's phase-2 kick also reduces
+ * its kinetic partials on the device and writes the record into mapped pinned
+ * host memory, so there is no host synchronisation per step.  kbt is the
+ * COM-subtracted temperature of compute_temperature (src/core.cpp:141-149) in
+ * one pass: (sum |v|^2 - |sum v|^2 / n) / (3 n); momentum = sum v. */
+int dpdb_step_thermo(dpdb_ctx* ctx, int64_t nsteps, dpdb_thermo* out);
 /* Runs nsteps like dpdb_step and returns the device time (CUDA events on the
  * context stream, ms).  stage_ms[0..5] (may be NULL): integrate, sort+permute,
  * build, force, other, total; stage_launches[0..5] likewise (kernel launches). */

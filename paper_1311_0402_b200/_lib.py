@@ -88,6 +88,7 @@ SYMBOLS = {
     "dpdb_setup": (C.c_int, [C.c_void_p]),
     "dpdb_step": (C.c_int, [C.c_void_p, C.c_int64]),
     "dpdb_thermo_get": (C.c_int, [C.c_void_p, C.POINTER(Thermo)]),
+    "dpdb_step_thermo": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(Thermo)]),
     "dpdb_step_timed": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_double), C.c_void_p,
                                   C.c_void_p]),
     "dpdb_current_step": (C.c_int64, [C.c_void_p]),

@@ -75,6 +75,11 @@ struct dpdb_ctx {
     bool has_mol = false, have_sorted = false, have_table = false, tiled = true, joined = false;
     bool multi = false;  // n_species > 1: species packed into pos4.w bits 28-31
     bool no_fuse = false;  // DPDB_FUSE=0: keep the Verlet pass a separate kernel (A/B)
+    // per-step thermo (dpdb_step_thermo): block partials of the phase-2 pass
+    // and the records, written by the device straight into mapped pinned memory
+    double* thermo_part{};
+    double *thermo_host{}, *thermo_host_dev{};
+    size_t thermo_cap = 0;  // records
     int64_t step = 0;
     std::string last_error;
     // stage timing
@@ -259,9 +264,10 @@ dpdb::IntegrateArgs integrate_args(dpdb_ctx* ctx, bool defer_wrap) {
 }
 
 template <bool P2, bool P1, bool KEYS, bool STREAMS>
-int launch_integrate(dpdb_ctx* ctx, bool defer_wrap = false) {
+int launch_integrate(dpdb_ctx* ctx, bool defer_wrap = false, bool thermo = false) {
     if (!ctx->n) return 0;
-    const dpdb::IntegrateArgs a = integrate_args(ctx, defer_wrap);
+    dpdb::IntegrateArgs a = integrate_args(ctx, defer_wrap);
+    if (P2 && thermo) a.thermo_part = ctx->thermo_part;
     dpdb::k_integrate<P2, P1, KEYS, STREAMS><<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(a);
     CKL();
     ctx->launches[ST_INTEGRATE]++;
@@ -500,7 +506,7 @@ bool can_fuse(const dpdb_ctx* ctx) {
 // fuse (step loop only, can_fuse): FUSE_STREAMS / FUSE_KEYS run phase 2 of
 // this step + phase 1 of the next in the force kernel's epilogue; the forces
 // themselves are then not stored.
-int do_forces(dpdb_ctx* ctx, uint32_t step, int fuse = dpdb::FUSE_NONE) {
+int do_forces(dpdb_ctx* ctx, uint32_t step, int fuse = dpdb::FUSE_NONE, bool thermo = false) {
     if (!ctx->have_table) return fail(ctx, DPDB_ECONFIG, "compute_forces: neighbor table not built");
     if (!ctx->n) return 0;
     const dpdb_params& p = ctx->params;
@@ -538,6 +544,7 @@ int do_forces(dpdb_ctx* ctx, uint32_t step, int fuse = dpdb::FUSE_NONE) {
     }
     if (fuse != dpdb::FUSE_NONE) {
         a.ia = integrate_args(ctx, false);
+        if (thermo) a.ia.thermo_part = ctx->thermo_part;
         a.pos4n = ctx->pos4n;
         a.vel4n = ctx->vel4n;
     }
@@ -775,7 +782,8 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         (rc = dalloc(ctx, ctx->md_mlist, ctx->md_valid ? 8 * c : 1)) ||
         (rc = dalloc(ctx, ctx->md_glist, ctx->md_valid ? 8 * c : 1)) ||
         (rc = dalloc(ctx, ctx->err, 1)) || (rc = dalloc(ctx, ctx->red, (size_t)RED_BLOCKS * 4)) ||
-        (rc = dalloc(ctx, ctx->red_out, 8)) || (rc = dalloc(ctx, ctx->tmp_u32, c)))
+        (rc = dalloc(ctx, ctx->red_out, 16)) || (rc = dalloc(ctx, ctx->tmp_u32, c)) ||
+        (rc = dalloc(ctx, ctx->thermo_part, 4 * (c / 256 + 1))))
         return bail(rc);
     ctx->md_list_cap = ctx->md_valid ? 8 * c : 1;  // a corner particle sits in 7 lists
     if (cudaMemset(ctx->err, 0, sizeof(DevErr)) != cudaSuccess ||
@@ -823,12 +831,13 @@ int dpdb_destroy(dpdb_ctx* ctx) {
                     ctx->vel4, ctx->pos4n, ctx->vel4n, ctx->keys, ctx->keys2, ctx->vals, ctx->vals2, ctx->hist,
                     ctx->cell_start, ctx->ostart, ctx->rank_of_cell, ctx->stencil, ctx->stencil_n,
                     ctx->cell_flags, ctx->stencil_code, ctx->cell_lo, ctx->entries, ctx->counts, ctx->fwalk, ctx->rowmeta,
-                    ctx->err, ctx->red, ctx->red_out,
+                    ctx->err, ctx->red, ctx->red_out, ctx->thermo_part,
                     ctx->tmp_u32, ctx->bond_off, ctx->bond_partner, ctx->index_of_tag,
                     ctx->bond_k, ctx->bond_r0, ctx->md_masks, ctx->md_mig, ctx->md_slot,
                     ctx->md_doff, ctx->md_dbase, ctx->md_mlist, ctx->md_glist};
     for (size_t q = 0; q < sizeof(ptrs) / sizeof(ptrs[0]); ++q)  // each buffer once
         if (ptrs[q] && std::find(ptrs, ptrs + q, ptrs[q]) == ptrs + q) cudaFree(ptrs[q]);
+    if (ctx->thermo_host) cudaFreeHost(ctx->thermo_host);
     for (int k = 0; k < 3; ++k) {
         void* q[] = {ctx->x[k], ctx->v[k], ctx->x2[k], ctx->v2[k], ctx->f[k], ctx->f2[k]};
         for (void* p : q)
@@ -1267,43 +1276,68 @@ namespace {
 // evaluations (phase 2 of step n + phase 1 of step n+1, plus the next step's
 // fp32 streams or sort keys) runs in the epilogue of step n's force kernel,
 // on the forces the block just reduced -- same arithmetic, one HBM pass fewer.
-int run_steps(dpdb_ctx* ctx, int64_t nsteps) {
+// rec (dpdb_step_thermo): device-visible record array, 5 doubles per step;
+// the pass that applies phase 2 of step n also reduces its thermo partials
+// and k_thermo_final writes record n -- no host synchronisation per step.
+int thermo_record(dpdb_ctx* ctx, uint32_t nblocks, double* rec) {
+    dpdb::k_thermo_final<<<1, 256, 0, ctx->stream>>>(ctx->thermo_part, nblocks, (uint32_t)ctx->n,
+                                                      ctx->step, rec);
+    CKL();
+    ctx->launches[ST_OTHER]++;
+    return 0;
+}
+
+int run_steps(dpdb_ctx* ctx, int64_t nsteps, double* rec = nullptr) {
     if (!ctx->have_table) return fail(ctx, DPDB_ECONFIG, "step: call dpdb_setup first");
+    const bool th = rec != nullptr;
+    const uint32_t nb_int = (uint32_t)((ctx->n + 255) / 256);
+    const uint32_t nb_force = (uint32_t)((ctx->n + dpdb::FORCE_BLOCK - 1) / dpdb::FORCE_BLOCK);
     bool integrated = false;  // this step's Verlet pass already ran in the last force kernel
     for (int64_t s = 0; s < nsteps; ++s) {
         ctx->step += 1;
         const bool rebuild = ctx->step % ctx->run.rebuild_every == 0;
         mark(ctx, ST_OTHER);
+        // the integrate kernel here applies phase 2 of the previous step (s > 0)
+        const bool th_prev = th && s > 0 && !integrated;
         if (rebuild) {
             if (!integrated) {
-                if (s > 0) TRY((launch_integrate<true, true, true, false>(ctx)));
+                if (s > 0) TRY((launch_integrate<true, true, true, false>(ctx, false, th_prev)));
                 else TRY((launch_integrate<false, true, true, false>(ctx)));
                 mark(ctx, ST_INTEGRATE);
             }
+        } else if (!integrated) {
+            if (s > 0) TRY((launch_integrate<true, true, false, true>(ctx, false, th_prev)));
+            else TRY((launch_integrate<false, true, false, true>(ctx)));
+            mark(ctx, ST_INTEGRATE);
+        }
+        if (th_prev) {
+            ctx->step -= 1;  // the record belongs to the previous step
+            TRY(thermo_record(ctx, nb_int, rec + 5 * (s - 1)));
+            ctx->step += 1;
+        }
+        if (rebuild) {
             TRY(do_sort(ctx));
             TRY(do_permute(ctx, false));
             mark(ctx, ST_SORT);
             TRY(do_build(ctx, true));
             mark(ctx, ST_BUILD);
-        } else if (!integrated) {
-            if (s > 0) TRY((launch_integrate<true, true, false, true>(ctx)));
-            else TRY((launch_integrate<false, true, false, true>(ctx)));
-            mark(ctx, ST_INTEGRATE);
         }
         const bool fuse = s + 1 < nsteps && can_fuse(ctx);
         const bool next_rebuild = (ctx->step + 1) % ctx->run.rebuild_every == 0;
         TRY(do_forces(ctx, (uint32_t)ctx->step,
-                      fuse ? (next_rebuild ? dpdb::FUSE_KEYS : dpdb::FUSE_STREAMS) : dpdb::FUSE_NONE));
+                      fuse ? (next_rebuild ? dpdb::FUSE_KEYS : dpdb::FUSE_STREAMS) : dpdb::FUSE_NONE, th));
         if (fuse && !next_rebuild) {
             std::swap(ctx->pos4, ctx->pos4n);
             std::swap(ctx->vel4, ctx->vel4n);
         }
         integrated = fuse;
         mark(ctx, ST_FORCE);
+        if (fuse && th) TRY(thermo_record(ctx, nb_force, rec + 5 * s));
     }
     if (nsteps > 0) {
-        TRY((launch_integrate<true, false, false, false>(ctx)));
+        TRY((launch_integrate<true, false, false, false>(ctx, false, th)));
         mark(ctx, ST_INTEGRATE);
+        if (th) TRY(thermo_record(ctx, nb_int, rec + 5 * (nsteps - 1)));
     }
     return 0;
 }
@@ -1315,6 +1349,34 @@ int dpdb_step(dpdb_ctx* ctx, int64_t nsteps) {
     CK(cudaSetDevice(ctx->device));
     TRY(run_steps(ctx, nsteps));
     return check_device(ctx);
+}
+
+int dpdb_step_thermo(dpdb_ctx* ctx, int64_t nsteps, dpdb_thermo* out) {
+    TRY(require_ctx(ctx));
+    CK(cudaSetDevice(ctx->device));
+    if (nsteps < 0) return fail(ctx, DPDB_ECONFIG, "step_thermo: nsteps must be >= 0");
+    if (!nsteps) return 0;
+    if (!ctx->n) return fail(ctx, DPDB_EPHYSICS, "temperature of an empty system");
+    if ((size_t)nsteps > ctx->thermo_cap) {
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (ctx->thermo_host) CK(cudaFreeHost(ctx->thermo_host));
+        ctx->thermo_host = nullptr;
+        ctx->thermo_cap = 0;
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&ctx->thermo_host), (size_t)nsteps * 5 * sizeof(double),
+                         cudaHostAllocMapped));
+        CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->thermo_host_dev), ctx->thermo_host, 0));
+        ctx->thermo_cap = (size_t)nsteps;
+    }
+    TRY(run_steps(ctx, nsteps, ctx->thermo_host_dev));
+    TRY(check_device(ctx));
+    for (int64_t s = 0; s < nsteps; ++s) {
+        const double* r = ctx->thermo_host + 5 * s;
+        out[s].step = (int64_t)r[0];
+        out[s].n = ctx->n;
+        out[s].kbt = r[1];
+        for (int k = 0; k < 3; ++k) out[s].momentum[k] = r[2 + k];
+    }
+    return 0;
 }
 
 int dpdb_step_timed(dpdb_ctx* ctx, int64_t nsteps, double* ms, double* stage_ms,
@@ -1356,17 +1418,15 @@ int dpdb_thermo_get(dpdb_ctx* ctx, dpdb_thermo* out) {
                                                       (uint32_t)ctx->n, ctx->red);
     dpdb::k_sum_partials<<<1, 32, 0, ctx->stream>>>(ctx->red, RED_BLOCKS, ctx->red_out);
     dpdb::k_mean_from_sum<<<1, 32, 0, ctx->stream>>>(ctx->red_out, 1.0 / (double)ctx->n);
-    double sums[8];
-    CK(cudaMemcpyAsync(sums, ctx->red_out, sizeof sums, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    // second pass around the device-resident mean; one read-back for both
     dpdb::k_sum3<<<RED_BLOCKS, 256, 0, ctx->stream>>>(ctx->v[0], ctx->v[1], ctx->v[2],
                                                       ctx->red_out + 4, (uint32_t)ctx->n, ctx->red);
-    dpdb::k_sum_partials<<<1, 32, 0, ctx->stream>>>(ctx->red, RED_BLOCKS, ctx->red_out);
-    double s2[8];
-    CK(cudaMemcpyAsync(s2, ctx->red_out, sizeof s2, cudaMemcpyDeviceToHost, ctx->stream));
+    dpdb::k_sum_partials<<<1, 32, 0, ctx->stream>>>(ctx->red, RED_BLOCKS, ctx->red_out + 8);
+    double r[16];
+    CK(cudaMemcpyAsync(r, ctx->red_out, sizeof r, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    for (int k = 0; k < 3; ++k) out->momentum[k] = sums[k];
-    out->kbt = s2[3] / (3.0 * (double)ctx->n);
+    for (int k = 0; k < 3; ++k) out->momentum[k] = r[k];
+    out->kbt = r[8 + 3] / (3.0 * (double)ctx->n);
     return 0;
 }
 

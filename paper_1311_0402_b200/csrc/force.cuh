@@ -549,6 +549,7 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceA
         }
     }
     __syncthreads();
+    double th[4] = {0.0, 0.0, 0.0, 0.0};  // FUSE: this thread's thermo partial
 #pragma unroll
     for (int q = 0; q < PER_T; ++q) {
         const uint32_t t = threadIdx.x + q * FORCE_WARPS * 32;
@@ -575,8 +576,15 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceA
             const int qq = FUSE ? q : 0;
             const double x[3] = {ex[qq][0], ex[qq][1], ex[qq][2]};
             const double v[3] = {ex[qq][3], ex[qq][4], ex[qq][5]};
+            double vf[3];
             integrate_particle<true, true, FUSE == FUSE_KEYS, FUSE == FUSE_STREAMS>(
-                a.ia, i, f, x, v, etag[qq], esp[qq], a.pos4n, a.vel4n);
+                a.ia, i, f, x, v, etag[qq], esp[qq], a.pos4n, a.vel4n, vf);
+            th[0] += vf[0];
+            th[1] += vf[1];
+            th[2] += vf[2];
+            th[3] += vf[0] * vf[0] + vf[1] * vf[1] + vf[2] * vf[2];
         }
     }
+    if (FUSE != FUSE_NONE && a.ia.thermo_part)  // uniform per launch
+        block_sum4<FORCE_WARPS * 32>(th, a.ia.thermo_part + 4 * blockIdx.x);
 }

@@ -140,7 +140,30 @@ struct IntegrateArgs {
     DevGrid grid;
     double dt, h;
     uint32_t n;
+    double* thermo_part;  // PHASE2 passes: per-block (sum v_x, v_y, v_z, |v|^2) of the full-step v, or null
 };
+
+// Fixed-order block sum of four fp64 values (one per thread) for the per-step
+// thermo: shuffle tree inside each warp, then warp 0 adds the warp sums in
+// warp order.  Deterministic for a given block shape.  All threads call it.
+template <int THREADS>
+__device__ __forceinline__ void block_sum4(double (&v)[4], double* out) {
+    __shared__ double ws[THREADS / 32][4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_down_sync(0xFFFFFFFFu, v[q], o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ws[w][q] = v[q];
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        double acc = 0.0;
+        for (int k = 0; k < THREADS / 32; ++k) acc += ws[k][threadIdx.x];
+        out[threadIdx.x] = acc;
+    }
+}
 
 // Fused Verlet: [phase 2 of the previous step] + phase 1 of this step +
 // boundary + either the sort keys (rebuild step; the permute kernel then
@@ -153,7 +176,7 @@ template <bool PHASE2, bool PHASE1, bool KEYS, bool STREAMS>
 __device__ __forceinline__ void integrate_particle(const IntegrateArgs& a, uint32_t i, const float f[3],
                                                    const double xin[3], const double vin[3],
                                                    uint32_t tag, uint32_t spc, float4* pos4,
-                                                   float4* vel4) {
+                                                   float4* vel4, double vfull[3]) {
     double xs[3], vs[3];
     bool ok = true;
 #pragma unroll
@@ -162,6 +185,7 @@ __device__ __forceinline__ void integrate_particle(const IntegrateArgs& a, uint3
         if (PHASE2 || PHASE1) {
             const double fk = (double)f[k];
             if (PHASE2) v = __dadd_rn(v, __dmul_rn(a.h, fk));
+            vfull[k] = v;  // the full-step velocity (after phase 2), for the thermo
             if (PHASE1) v = __dadd_rn(v, __dmul_rn(a.h, fk));
         }
         double x = xin[k];
@@ -197,18 +221,47 @@ __device__ __forceinline__ void integrate_particle(const IntegrateArgs& a, uint3
 template <bool PHASE2, bool PHASE1, bool KEYS, bool STREAMS>
 __global__ void __launch_bounds__(256) k_integrate(IntegrateArgs a) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= a.n) return;
-    float f[3] = {0.f, 0.f, 0.f};
-    double x[3], v[3];
+    double vf[3] = {0.0, 0.0, 0.0};
+    if (i < a.n) {
+        float f[3] = {0.f, 0.f, 0.f};
+        double x[3], v[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        if (PHASE2 || PHASE1) f[k] = a.f[k][i];
-        x[k] = a.x[k][i];
-        v[k] = a.v[k][i];
+        for (int k = 0; k < 3; ++k) {
+            if (PHASE2 || PHASE1) f[k] = a.f[k][i];
+            x[k] = a.x[k][i];
+            v[k] = a.v[k][i];
+        }
+        const uint32_t tag = (STREAMS || PHASE1) ? a.tag[i] : 0u;  // signature / error report
+        const uint32_t spc = (STREAMS && a.sp) ? a.sp[i] : 0u;
+        integrate_particle<PHASE2, PHASE1, KEYS, STREAMS>(a, i, f, x, v, tag, spc, a.pos4, a.vel4, vf);
     }
-    const uint32_t tag = (STREAMS || PHASE1) ? a.tag[i] : 0u;  // signature / error report
-    const uint32_t spc = (STREAMS && a.sp) ? a.sp[i] : 0u;
-    integrate_particle<PHASE2, PHASE1, KEYS, STREAMS>(a, i, f, x, v, tag, spc, a.pos4, a.vel4);
+    if (PHASE2 && a.thermo_part) {  // uniform per launch
+        double s4[4] = {vf[0], vf[1], vf[2], vf[0] * vf[0] + vf[1] * vf[1] + vf[2] * vf[2]};
+        block_sum4<256>(s4, a.thermo_part + 4 * blockIdx.x);
+    }
+}
+
+// Per-step thermo record from the block partials of the pass that applied
+// phase 2 (fixed order): rec = {step, kT, P_x, P_y, P_z} with
+// kT = (sum |v|^2 - |sum v|^2 / n) / (3 n), the COM-subtracted temperature of
+// compute_temperature (src/core.cpp:141-149) in one pass.
+__global__ void __launch_bounds__(256) k_thermo_final(const double* part, uint32_t nblocks, uint32_t n,
+                                                      int64_t step, double* rec) {
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    for (uint32_t b = threadIdx.x; b < nblocks; b += 256)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] += part[4 * b + q];
+    __shared__ double tot[4];
+    block_sum4<256>(v, tot);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const double p2 = tot[0] * tot[0] + tot[1] * tot[1] + tot[2] * tot[2];
+        rec[0] = (double)step;
+        rec[1] = (tot[3] - p2 / (double)n) / (3.0 * (double)n);
+        rec[2] = tot[0];
+        rec[3] = tot[1];
+        rec[4] = tot[2];
+    }
 }
 
 // ------------------------------------------------------- radix sort

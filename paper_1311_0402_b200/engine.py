@@ -249,6 +249,16 @@ class Engine:
         self._check(lib().dpdb_download(self.h, *[ptr(x) for x in a], ptr(tag), ptr(sp), ptr(sig)))
         return ParticleStore(a[0:3], a[3:6], tag, sp, None, a[6:9], sig)
 
+    def download_state(self, coord, veloc):
+        """Positions and velocities into caller-owned float64 arrays (e.g.
+        pinned buffers: no staging copy); the other fields are skipped."""
+        arrs = list(coord) + list(veloc)
+        for a in arrs:
+            if a.dtype != np.float64 or not a.flags.c_contiguous or len(a) < self.n:
+                raise ValueError("download_state: contiguous float64 arrays of length >= n")
+        self._check(lib().dpdb_download(self.h, *[ptr(x) for x in arrs], None, None, None,
+                                        None, None, None))
+
     def set_bonds(self, tag_i, tag_j, k, r0):
         ti, tj = (np.ascontiguousarray(t, np.uint32) for t in (tag_i, tag_j))
         kk, rr = (np.ascontiguousarray(np.broadcast_to(np.asarray(v, np.float64), ti.shape))
@@ -335,6 +345,17 @@ class Engine:
 
     def step(self, nsteps: int = 1):
         self._check(lib().dpdb_step(self.h, int(nsteps)))
+
+    def step_thermo(self, nsteps: int):
+        """dpdb_step_thermo: run nsteps and return every step's thermo line as
+        arrays (step, kbt, momentum[n, 3]); the records are reduced on the
+        device and land in pinned host memory without a per-step sync."""
+        recs = (Thermo * max(int(nsteps), 1))()
+        self._check(lib().dpdb_step_thermo(self.h, int(nsteps), recs))
+        k = int(nsteps)
+        return dict(step=np.array([recs[i].step for i in range(k)], np.int64),
+                    kbt=np.array([recs[i].kbt for i in range(k)]),
+                    momentum=np.array([tuple(recs[i].momentum) for i in range(k)]).reshape(k, 3))
 
     def step_timed(self, nsteps: int, stages: bool = False):
         ms = C.c_double()

@@ -183,3 +183,32 @@ def test_c3_properties_4m():
     rms = np.sqrt((F ** 2).sum(1).mean())
     assert np.abs(F.sum(0)).max() < 1e-5 * rms * np.sqrt(n)
     assert abs(e.thermo()["kbt"] - 1.0) < 0.05
+
+
+@pytest.mark.parametrize("fuse", ["1", "0"])
+def test_step_thermo_records(monkeypatch, fuse):
+    """dpdb_step_thermo: every step's thermo line is reduced on the device by
+    the pass that applies that step's phase-2 kick (fused force epilogue or the
+    separate Verlet pass); the records match dpdb_thermo_get after each single
+    step, and the trajectory is the one dpdb_step gives."""
+    monkeypatch.setenv("DPDB_FUSE", fuse)
+    box, obox, st = _sys.fluid((12, 12, 12), 3.0, seed=31)
+    a = _sys.engine(box, st, run=dpd.RunConfig(rebuild_every=4))
+    b = _sys.engine(box, st, run=dpd.RunConfig(rebuild_every=4))
+    a.setup()
+    b.setup()
+    ref = []
+    for _ in range(11):
+        a.step(1)
+        ref.append(a.thermo())
+    rec = b.step_thermo(11)
+    assert list(rec["step"]) == [t["step"] for t in ref]
+    n = len(st[0])
+    for k, t in enumerate(ref):
+        assert abs(rec["kbt"][k] - t["kbt"]) <= 1e-12 * t["kbt"]
+        assert np.allclose(rec["momentum"][k], t["momentum"], rtol=0, atol=1e-9 * n)
+    sa, sb = a.download(), b.download()
+    for u, w in zip(sa.coord + sa.veloc + sa.force, sb.coord + sb.veloc + sb.force):
+        assert np.array_equal(u, w)
+    rec2 = b.step_thermo(3)  # a second call continues the step count
+    assert list(rec2["step"]) == [12, 13, 14]
