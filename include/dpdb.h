@@ -236,6 +236,9 @@ int dpdb_md_finish(dpdb_ctx* ctx);
 /* sum of v, v^2 over the locals (for a cross-brick temperature) */
 int dpdb_md_sums(dpdb_ctx* ctx, double out[4]);
 int dpdb_md_ghost_count(const dpdb_ctx* ctx, size_t* ng);
+/* force blocks of the current table and how many of them are interior (no
+ * ghost partner: their forces run while the ghost update is in flight) */
+int dpdb_md_block_split(dpdb_ctx* ctx, size_t* n_blocks, size_t* n_interior);
 /* the ghosts [n, n + ng) as this brick holds them (x shifted to its image) */
 int dpdb_md_download_ghosts(dpdb_ctx* ctx, double* x, double* y, double* z, double* vx,
                             double* vy, double* vz, uint32_t* tag);

@@ -114,6 +114,7 @@ SYMBOLS = {
     "dpdb_md_finish": (C.c_int, [C.c_void_p]),
     "dpdb_md_sums": (C.c_int, [C.c_void_p, C.c_void_p]),
     "dpdb_md_ghost_count": (C.c_int, [C.c_void_p, C.POINTER(C.c_size_t)]),
+    "dpdb_md_block_split": (C.c_int, [C.c_void_p, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
     "dpdb_md_download_ghosts": (C.c_int, [C.c_void_p] + [C.c_void_p] * 7),
     "dpdb_group_setup": (C.c_int, [C.c_void_p, C.c_int]),
     "dpdb_group_step": (C.c_int, [C.c_void_p, C.c_int, C.c_int64]),

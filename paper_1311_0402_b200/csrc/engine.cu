@@ -38,6 +38,11 @@ enum Stage { ST_INTEGRATE = 0, ST_SORT = 1, ST_BUILD = 2, ST_FORCE = 3, ST_OTHER
 struct dpdb_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    // bricks: the ghost update runs on halo_stream while the interior force
+    // blocks run on stream (ev_pack: send records packed; ev_halo: ghosts in)
+    cudaStream_t halo_stream = nullptr;
+    cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
+    uint8_t* blk_ghost{};  // per force block: 1 if any row has a ghost partner (set by the builder)
     dpdb_box box{};
     dpdb_params params{};
     dpdb_run run{};
@@ -411,6 +416,7 @@ int do_build(dpdb_ctx* ctx, bool joined_out) {
     a.cut_s = (float)(rs * rs);
     wrap_lengths(ctx, a.L, a.H);
     if (ctx->builder == 2) {
+        a.blk_ghost = ctx->blk_ghost;
         a.stencil_code = ctx->stencil_code;
         a.cell_lo = ctx->cell_lo;
         for (int k = 0; k < 3; ++k) a.csz[k] = (float)ctx->grid.cell_size[k];
@@ -425,6 +431,9 @@ int do_build(dpdb_ctx* ctx, bool joined_out) {
         ctx->launches[ST_BUILD]++;
         return 0;
     }
+    // other builders do not flag ghost-partner blocks: mark every block
+    // boundary so an interior/boundary split computes everything after the halo
+    CK(cudaMemsetAsync(ctx->blk_ghost, 1, ctx->n / dpdb::FORCE_BLOCK + 1, ctx->stream));
     if (ctx->builder == 1) {
         if (joined_out)
             dpdb::k_build_lane<true><<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(a);
@@ -506,7 +515,10 @@ bool can_fuse(const dpdb_ctx* ctx) {
 // fuse (step loop only, can_fuse): FUSE_STREAMS / FUSE_KEYS run phase 2 of
 // this step + phase 1 of the next in the force kernel's epilogue; the forces
 // themselves are then not stored.
-int do_forces(dpdb_ctx* ctx, uint32_t step, int fuse = dpdb::FUSE_NONE, bool thermo = false) {
+// part (bricks, walk layout): -1 every block; 0 the interior blocks (no ghost
+// partner: they can run while the ghost update is in flight); 1 the rest
+int do_forces(dpdb_ctx* ctx, uint32_t step, int fuse = dpdb::FUSE_NONE, bool thermo = false,
+              int part = -1) {
     if (!ctx->have_table) return fail(ctx, DPDB_ECONFIG, "compute_forces: neighbor table not built");
     if (!ctx->n) return 0;
     const dpdb_params& p = ctx->params;
@@ -541,6 +553,10 @@ int do_forces(dpdb_ctx* ctx, uint32_t step, int fuse = dpdb::FUSE_NONE, bool the
         a.ta[q] = (float)p.a[q];
         a.tg[q] = (float)p.gamma[q];
         a.ts[q] = (float)(ctx->sigma[q] / std::sqrt(p.dt));
+    }
+    if (part >= 0) {
+        a.blk_sel = ctx->blk_ghost;
+        a.sel_val = (uint32_t)part;
     }
     if (fuse != dpdb::FUSE_NONE) {
         a.ia = integrate_args(ctx, false);
@@ -744,7 +760,10 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         return code;
     };
     if (cudaSetDevice(device) != cudaSuccess) return bail(fail(ctx, DPDB_EDEVICE, "cudaSetDevice"));
-    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess)
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->halo_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_pack, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming) != cudaSuccess)
         return bail(fail(ctx, DPDB_EDEVICE, "cudaStreamCreate"));
     ctx->cap = std::max<size_t>(capacity, 1);
     ctx->n_pad = (ctx->cap + 31) & ~(size_t)31;
@@ -783,7 +802,8 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         (rc = dalloc(ctx, ctx->md_glist, ctx->md_valid ? 8 * c : 1)) ||
         (rc = dalloc(ctx, ctx->err, 1)) || (rc = dalloc(ctx, ctx->red, (size_t)RED_BLOCKS * 4)) ||
         (rc = dalloc(ctx, ctx->red_out, 16)) || (rc = dalloc(ctx, ctx->tmp_u32, c)) ||
-        (rc = dalloc(ctx, ctx->thermo_part, 4 * (c / 256 + 1))))
+        (rc = dalloc(ctx, ctx->thermo_part, 4 * (c / 256 + 1))) ||
+        (rc = dalloc(ctx, ctx->blk_ghost, c / dpdb::FORCE_BLOCK + 1)))
         return bail(rc);
     ctx->md_list_cap = ctx->md_valid ? 8 * c : 1;  // a corner particle sits in 7 lists
     if (cudaMemset(ctx->err, 0, sizeof(DevErr)) != cudaSuccess ||
@@ -831,7 +851,7 @@ int dpdb_destroy(dpdb_ctx* ctx) {
                     ctx->vel4, ctx->pos4n, ctx->vel4n, ctx->keys, ctx->keys2, ctx->vals, ctx->vals2, ctx->hist,
                     ctx->cell_start, ctx->ostart, ctx->rank_of_cell, ctx->stencil, ctx->stencil_n,
                     ctx->cell_flags, ctx->stencil_code, ctx->cell_lo, ctx->entries, ctx->counts, ctx->fwalk, ctx->rowmeta,
-                    ctx->err, ctx->red, ctx->red_out, ctx->thermo_part,
+                    ctx->err, ctx->red, ctx->red_out, ctx->thermo_part, ctx->blk_ghost,
                     ctx->tmp_u32, ctx->bond_off, ctx->bond_partner, ctx->index_of_tag,
                     ctx->bond_k, ctx->bond_r0, ctx->md_masks, ctx->md_mig, ctx->md_slot,
                     ctx->md_doff, ctx->md_dbase, ctx->md_mlist, ctx->md_glist};
@@ -845,6 +865,9 @@ int dpdb_destroy(dpdb_ctx* ctx) {
     }
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->halo_stream) cudaStreamDestroy(ctx->halo_stream);
+    if (ctx->ev_pack) cudaEventDestroy(ctx->ev_pack);
+    if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
     delete ctx;
     return 0;
 }

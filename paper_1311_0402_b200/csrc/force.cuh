@@ -35,6 +35,10 @@ struct ForceArgs {
     IntegrateArgs ia;
     float4* pos4n;
     float4* vel4n;
+    // bricks: run only the blocks with blk_sel[block] == sel_val (interior /
+    // boundary split around the ghost update); null = every block
+    const uint8_t* blk_sel;
+    uint32_t sel_val;
 };
 
 enum ForceFuse : int { FUSE_NONE = 0, FUSE_STREAMS = 1, FUSE_KEYS = 2 };
@@ -346,6 +350,7 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceA
     __shared__ float4 own_v[FORCE_WARPS][32];
     __shared__ uint32_t own_fl[FORCE_WARPS][32];
     __shared__ int acc[FORCE_BLOCK * 3];
+    if (a.blk_sel && a.blk_sel[blockIdx.x] != a.sel_val) return;  // whole CTA
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t b0 = blockIdx.x * FORCE_BLOCK;
     const uint32_t bn = min((uint32_t)FORCE_BLOCK, a.n - b0);

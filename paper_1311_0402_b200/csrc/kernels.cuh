@@ -532,6 +532,7 @@ struct BuildArgs {
     // k_build_range only: per-slot stencil offset codes and the cell boxes
     const uint8_t* stencil_code;  // [n_local_cells][32]: (ox+1) | (oy+1) << 2 | (oz+1) << 4, 0xFF = never cull
     const float4* cell_lo;        // [n_local_cells]: lower corner in the pos4 frame
+    uint8_t* blk_ghost;           // per force block: any row with a ghost partner (j >= n_local)
     float csz[3];                 // cell side per axis (fp32)
     float cut_cull;               // (r_c + skin + margin)^2
 };
@@ -895,8 +896,10 @@ __global__ void __launch_bounds__(RB_THREADS, 4) k_build_range(BuildArgs a) {
     const uint32_t bn = min((uint32_t)RB_BLOCK, a.n_local - b0);
     const uint32_t bend = b0 + bn;
     const uint32_t maxn = a.maxn;
+    __shared__ uint32_t ghost_seen;
     if (WALK)
         for (uint32_t q = t; q < RB_BLOCK; q += RB_THREADS) back[q] = 0;
+    if (t == 0) ghost_seen = 0u;
     __syncthreads();
     uint32_t cnt[RB_BLOCK / RB_THREADS];  // nc | nsk << 16 per pass
     uint32_t kfs[RB_BLOCK / RB_THREADS];
@@ -1049,6 +1052,7 @@ __global__ void __launch_bounds__(RB_THREADS, 4) k_build_range(BuildArgs a) {
                 __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
             const bool hit = v && d2 <= cut_s;
             const bool core = d2 <= cut_c;
+            if (hit && j >= a.n_local) ghost_seen = 1u;  // same value from every writer
             if (WALK) {
                 if (hit && kf < maxn) rowp[(kf & 31u) * maxn + (kf & ~31u)] = core ? j : (j | 0x80000000u);
                 kf += hit;
@@ -1073,7 +1077,8 @@ __global__ void __launch_bounds__(RB_THREADS, 4) k_build_range(BuildArgs a) {
         cnt[pass] = nc | (nsk << 16);
         kfs[pass] = kf;
     }
-    if (WALK) __syncthreads();
+    __syncthreads();
+    if (t == 0 && a.blk_ghost) a.blk_ghost[blockIdx.x] = ghost_seen ? 1 : 0;
 #pragma unroll
     for (int pass = 0; pass < RB_BLOCK / RB_THREADS; ++pass) {
         const uint32_t i = b0 + pass * RB_THREADS + t;

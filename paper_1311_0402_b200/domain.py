@@ -163,6 +163,12 @@ class _Brick(Engine):
         self._check(lib().dpdb_md_ghost_count(self.h, C.byref(n)))
         return n.value
 
+    def block_split(self):
+        """(force blocks, interior blocks) of the current table."""
+        nb, ni = C.c_size_t(), C.c_size_t()
+        self._check(lib().dpdb_md_block_split(self.h, C.byref(nb), C.byref(ni)))
+        return nb.value, ni.value
+
     def ghosts(self):
         """(x[3], v[3], tag) of the ghosts this brick holds."""
         ng = self.ghost_count

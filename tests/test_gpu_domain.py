@@ -166,6 +166,31 @@ def test_trajectory_matches_single_domain_without_noise(dims):
     g.close()
 
 
+@pytest.mark.parametrize("L,dims", [((40, 24, 24), (2, 1, 1)), ((36, 36, 36), (2, 2, 2)),
+                                    ((14, 13, 12), (3, 2, 1))])
+def test_overlapped_halo_update_is_bitwise_blocking(monkeypatch, L, dims):
+    """Between rebuilds the ghost update runs on a halo stream while the
+    interior force blocks (no ghost partner, flagged by the range builder)
+    compute; the boundary blocks wait for the ghosts.  Same forces and
+    trajectory bit for bit as the blocking update (DPDB_OVERLAP=0)."""
+    box, obox, st = _sys.fluid(L, 3.0, seed=41)
+    run = dpd.RunConfig(rebuild_every=4)
+    out = []
+    for ov in ("1", "0"):
+        monkeypatch.setenv("DPDB_OVERLAP", ov)
+        g = group(box, st, run, dims)
+        g.step(9)
+        if ov == "1" and L[0] >= 36:  # bricks large enough to have interior blocks
+            split = [b.block_split() for b in g.bricks]
+            assert all(ni < nb for nb, ni in split) and sum(ni for _, ni in split) > 0, split
+        out.append(g.download())
+        g.close()
+    a, b = out
+    assert np.array_equal(a.tag, b.tag)
+    for u, w in zip(a.coord + a.veloc + a.force, b.coord + b.veloc + b.force):
+        assert np.array_equal(u, w)
+
+
 def test_ghosts_are_shifted_copies_of_their_owners():
     """After setup, after ghost updates and after a rebuild every ghost
     holds its owner's x (+ a periodic image shift) and v exactly."""
