@@ -157,6 +157,19 @@ int dpdb_setup(dpdb_ctx* ctx);
 /* nsteps of Alg. 1's main loop; rebuild every rebuild_every */
 int dpdb_step(dpdb_ctx* ctx, int64_t nsteps);
 int dpdb_thermo_get(dpdb_ctx* ctx, dpdb_thermo* out);
+
+/* Validation observables.
+ * velocity_profile: nbins slabs of the box along bin_axis; each sample adds
+ * every particle's vel_axis velocity (2^-24 fixed point, bitwise reproducible)
+ * and a count to its slab.  get returns per-slab velocity sums and counts
+ * accumulated over nsamples samples (mean = sum / count; the double-Poiseuille
+ * fold and the viscosity fit are host-side, paper_1311_0402_b200.observables). */
+int dpdb_profile_reset(dpdb_ctx* ctx, uint32_t nbins, int32_t bin_axis, int32_t vel_axis);
+int dpdb_profile_sample(dpdb_ctx* ctx);
+int dpdb_profile_get(dpdb_ctx* ctx, double* sum_v, uint64_t* count, int64_t* nsamples);
+/* histogram of pair distances r < rmax <= r_c + skin over the current neighbor
+ * table, every pair once, fp32 distance of the builder (RDF numerator) */
+int dpdb_rdf(dpdb_ctx* ctx, uint32_t nbins, double rmax, uint64_t* hist);
 /* Runs nsteps like dpdb_step and records the thermo line of every step
  * (out[0..nsteps-1]): the pass that applies a step's phase-2 kick also reduces
  * its kinetic partials on the device and writes the record into mapped pinned

@@ -89,6 +89,10 @@ SYMBOLS = {
     "dpdb_step": (C.c_int, [C.c_void_p, C.c_int64]),
     "dpdb_thermo_get": (C.c_int, [C.c_void_p, C.POINTER(Thermo)]),
     "dpdb_step_thermo": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(Thermo)]),
+    "dpdb_profile_reset": (C.c_int, [C.c_void_p, C.c_uint32, C.c_int32, C.c_int32]),
+    "dpdb_profile_sample": (C.c_int, [C.c_void_p]),
+    "dpdb_profile_get": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]),
+    "dpdb_rdf": (C.c_int, [C.c_void_p, C.c_uint32, C.c_double, C.c_void_p]),
     "dpdb_step_timed": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_double), C.c_void_p,
                                   C.c_void_p]),
     "dpdb_current_step": (C.c_int64, [C.c_void_p]),

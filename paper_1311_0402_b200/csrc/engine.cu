@@ -43,6 +43,11 @@ struct dpdb_ctx {
     cudaStream_t halo_stream = nullptr;
     cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
     uint8_t* blk_ghost{};  // per force block: 1 if any row has a ghost partner (set by the builder)
+    // velocity_profile accumulators: 2 * nbins u64 (fixed-point sums, counts)
+    unsigned long long* prof_acc{};
+    uint32_t prof_nbins = 0;
+    int prof_bin_axis = 2, prof_vel_axis = 0;
+    int64_t prof_samples = 0;
     dpdb_box box{};
     dpdb_params params{};
     dpdb_run run{};
@@ -851,7 +856,7 @@ int dpdb_destroy(dpdb_ctx* ctx) {
                     ctx->vel4, ctx->pos4n, ctx->vel4n, ctx->keys, ctx->keys2, ctx->vals, ctx->vals2, ctx->hist,
                     ctx->cell_start, ctx->ostart, ctx->rank_of_cell, ctx->stencil, ctx->stencil_n,
                     ctx->cell_flags, ctx->stencil_code, ctx->cell_lo, ctx->entries, ctx->counts, ctx->fwalk, ctx->rowmeta,
-                    ctx->err, ctx->red, ctx->red_out, ctx->thermo_part, ctx->blk_ghost,
+                    ctx->err, ctx->red, ctx->red_out, ctx->thermo_part, ctx->blk_ghost, ctx->prof_acc,
                     ctx->tmp_u32, ctx->bond_off, ctx->bond_partner, ctx->index_of_tag,
                     ctx->bond_k, ctx->bond_r0, ctx->md_masks, ctx->md_mig, ctx->md_slot,
                     ctx->md_doff, ctx->md_dbase, ctx->md_mlist, ctx->md_glist};
@@ -1429,6 +1434,99 @@ int dpdb_table_stats(dpdb_ctx* ctx, double* mean_row, double* mean_core, uint32_
     if (mean_core) *mean_core = sc * inv;
     if (max_row) *max_row = mx;
     return 0;
+}
+
+// ------------------------------------------------ validation observables
+int dpdb_profile_reset(dpdb_ctx* ctx, uint32_t nbins, int32_t bin_axis, int32_t vel_axis) {
+    TRY(require_ctx(ctx));
+    CK(cudaSetDevice(ctx->device));
+    if (nbins < 1 || nbins > (uint32_t)dpdb::PROF_MAX_BINS)
+        return fail(ctx, DPDB_ECONFIG, "velocity_profile: 1..1024 bins");
+    if (bin_axis < 0 || bin_axis > 2 || vel_axis < 0 || vel_axis > 2)
+        return fail(ctx, DPDB_ECONFIG, "velocity_profile: axes must be 0, 1 or 2");
+    if (nbins > ctx->prof_nbins) {
+        if (ctx->prof_acc) CK(cudaFree(ctx->prof_acc));
+        ctx->prof_acc = nullptr;
+        ctx->prof_nbins = 0;
+        CK(cudaMalloc(&ctx->prof_acc, 2 * (size_t)nbins * sizeof(unsigned long long)));
+    }
+    ctx->prof_nbins = nbins;
+    ctx->prof_bin_axis = bin_axis;
+    ctx->prof_vel_axis = vel_axis;
+    ctx->prof_samples = 0;
+    CK(cudaMemsetAsync(ctx->prof_acc, 0, 2 * (size_t)nbins * sizeof(unsigned long long), ctx->stream));
+    return 0;
+}
+
+int dpdb_profile_sample(dpdb_ctx* ctx) {
+    TRY(require_ctx(ctx));
+    CK(cudaSetDevice(ctx->device));
+    if (!ctx->prof_nbins) return fail(ctx, DPDB_ECONFIG, "velocity_profile: call dpdb_profile_reset first");
+    const int ba = ctx->prof_bin_axis;
+    const double lo = ctx->box.lo[ba], w = (ctx->box.hi[ba] - ctx->box.lo[ba]) / ctx->prof_nbins;
+    if (ctx->n) {
+        const unsigned nb = std::min<unsigned>(blocks_for(ctx->n, 256), 4 * 148);
+        dpdb::k_profile<<<nb, 256, 0, ctx->stream>>>(ctx->x[ba], ctx->v[ctx->prof_vel_axis],
+                                                     (uint32_t)ctx->n, lo, 1.0 / w, ctx->prof_nbins,
+                                                     ctx->prof_acc);
+        CKL();
+        ctx->launches[ST_OTHER]++;
+    }
+    ctx->prof_samples += 1;
+    return check_device(ctx);
+}
+
+int dpdb_profile_get(dpdb_ctx* ctx, double* sum_v, uint64_t* count, int64_t* nsamples) {
+    TRY(require_ctx(ctx));
+    CK(cudaSetDevice(ctx->device));
+    const uint32_t nb = ctx->prof_nbins;
+    if (!nb) return fail(ctx, DPDB_ECONFIG, "velocity_profile: call dpdb_profile_reset first");
+    std::vector<unsigned long long> h(2 * (size_t)nb);
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(h.data(), ctx->prof_acc, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    for (uint32_t b = 0; b < nb; ++b) {
+        if (sum_v) sum_v[b] = (double)(long long)h[b] / dpdb::PROF_SCALE;
+        if (count) count[b] = h[nb + b];
+    }
+    if (nsamples) *nsamples = ctx->prof_samples;
+    return 0;
+}
+
+int dpdb_rdf(dpdb_ctx* ctx, uint32_t nbins, double rmax, uint64_t* hist) {
+    TRY(require_ctx(ctx));
+    CK(cudaSetDevice(ctx->device));
+    if (!ctx->have_table) return fail(ctx, DPDB_ECONFIG, "rdf: neighbor table not built");
+    if (nbins < 1 || nbins > 8192) return fail(ctx, DPDB_ECONFIG, "rdf: 1..8192 bins");
+    if (!(rmax > 0) || rmax > ctx->params.r_c + ctx->run.skin + 1e-12)
+        return fail(ctx, DPDB_ECONFIG, "rdf: 0 < rmax <= r_c + skin (the table's reach)");
+    if (ctx->walk == 1 || ctx->walk == 2) TRY(unwalk(ctx));  // lane/ballot walk orders: back to reference rows
+    unsigned long long* d = reinterpret_cast<unsigned long long*>(ctx->tmp_u32);
+    if ((size_t)nbins * 2 > ctx->n_pad) return fail(ctx, DPDB_ECONFIG, "rdf: more bins than scratch");
+    CK(cudaMemsetAsync(d, 0, nbins * sizeof(unsigned long long), ctx->stream));
+    if (ctx->n) {
+        dpdb::RdfArgs a{};
+        a.pos4 = ctx->pos4;
+        a.entries = ctx->entries;
+        a.counts = ctx->counts;
+        a.fwalk = ctx->fwalk;
+        a.n = (uint32_t)ctx->n;
+        a.maxn = ctx->maxn;
+        a.nbins = nbins;
+        a.layout = ctx->walk == 3 ? 3 : 0;
+        a.tiled = ctx->tiled;
+        a.joined = ctx->joined;
+        for (int k = 0; k < 3; ++k) a.wrap[k] = ctx->grid.wrap[k];
+        wrap_lengths(ctx, a.L, a.H);
+        a.bins_per_r = (float)(nbins / rmax);
+        dpdb::k_rdf<<<blocks_for(ctx->n, 256), 256, nbins * 4, ctx->stream>>>(a, d);
+        CKL();
+        ctx->launches[ST_OTHER]++;
+    }
+    std::vector<unsigned long long> h(nbins);
+    CK(cudaMemcpyAsync(h.data(), d, nbins * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (uint32_t b = 0; b < nbins; ++b) hist[b] = h[b];
+    return check_device(ctx);
 }
 
 int dpdb_thermo_get(dpdb_ctx* ctx, dpdb_thermo* out) {

@@ -1225,6 +1225,96 @@ __global__ void k_mean_from_sum(double* sum, double inv_n) {
     if (threadIdx.x < 3) sum[4 + threadIdx.x] = sum[threadIdx.x] * inv_n;
 }
 
+// ------------------------------------------------ validation observables
+// velocity_profile: per-bin sums of the drive-axis velocity and
+// particle counts along the profile axis.  Velocities are accumulated as
+// 2^-24 fixed point in int64 (shared, then global): integer sums commute, so
+// the profile is bitwise reproducible whatever the launch order.
+constexpr double PROF_SCALE = 16777216.0;  // 2^24
+constexpr int PROF_MAX_BINS = 1024;
+
+__global__ void __launch_bounds__(256) k_profile(const double* __restrict__ xb,
+                                                 const double* __restrict__ vd, uint32_t n, double lo,
+                                                 double inv_w, uint32_t nbins,
+                                                 unsigned long long* acc) {
+    __shared__ unsigned long long s_sum[PROF_MAX_BINS];
+    __shared__ unsigned int s_cnt[PROF_MAX_BINS];
+    for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x) {
+        s_sum[b] = 0ull;
+        s_cnt[b] = 0u;
+    }
+    __syncthreads();
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double f = floor((xb[i] - lo) * inv_w);
+        const uint32_t b = f < 0.0 ? 0u : (f >= (double)nbins ? nbins - 1u : (uint32_t)f);
+        const long long q = __double2ll_rn(vd[i] * PROF_SCALE);
+        atomicAdd(&s_sum[b], (unsigned long long)q);  // two's complement: signed sums wrap correctly
+        atomicAdd(&s_cnt[b], 1u);
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x) {
+        if (s_cnt[b]) {
+            atomicAdd(&acc[b], s_sum[b]);
+            atomicAdd(&acc[nbins + b], (unsigned long long)s_cnt[b]);
+        }
+    }
+}
+
+// Pair-distance histogram of the current neighbor table (radial distribution
+// numerator): every pair once (the entry with j > i), fp32 distance on the
+// pos4 frame with the fp32 minimum image of the builder, bin = floor(r *
+// nbins / rmax) in fp32 (r = IEEE sqrt).  layout 0: reference rows (split or
+// joined, tiled or not); layout 3: range-walk front entries (bit 31 = skin).
+struct RdfArgs {
+    const float4* pos4;
+    const uint32_t* entries;
+    const uint32_t* counts;
+    const uint32_t* fwalk;
+    uint32_t n, maxn, nbins;
+    int layout, tiled, joined;
+    int wrap[3];
+    float L[3], H[3];
+    float bins_per_r;
+};
+
+__global__ void __launch_bounds__(256) k_rdf(RdfArgs a, unsigned long long* hist) {
+    extern __shared__ unsigned int s_h[];
+    for (uint32_t b = threadIdx.x; b < a.nbins; b += blockDim.x) s_h[b] = 0u;
+    __syncthreads();
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < a.n) {
+        const float4 pi = a.pos4[i];
+        uint32_t nf, nc = 0;
+        if (a.layout == 3) {
+            nf = min(a.fwalk[i] & 0x1FFFu, a.maxn);
+        } else {
+            nc = a.counts[i] & 0x1FFFu;
+            nf = min(nc + ((a.counts[i] >> 13) & 0x1FFFu), a.maxn);
+        }
+        for (uint32_t m = 0; m < nf; ++m) {
+            uint32_t k = m;
+            if (a.layout == 0 && !a.joined && m >= nc) k = a.maxn - 1u - (m - nc);  // skin from the back
+            const size_t off = a.tiled ? (size_t)((i & ~31u) + (k & 31u)) * a.maxn + (k & ~31u) + (i & 31u)
+                                       : (size_t)i * a.maxn + k;
+            const uint32_t j = a.entries[off] & 0x7FFFFFFFu;
+            if (j <= i) continue;
+            const float4 pj = a.pos4[j];
+            float d[3] = {__fsub_rn(pi.x, pj.x), __fsub_rn(pi.y, pj.y), __fsub_rn(pi.z, pj.z)};
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+                if (a.wrap[q]) d[q] = min_image_f(d[q], a.L[q], a.H[q]);
+            const float r2 = __fadd_rn(__fadd_rn(__fmul_rn(d[0], d[0]), __fmul_rn(d[1], d[1])),
+                                       __fmul_rn(d[2], d[2]));
+            const float r = __fsqrt_rn(r2);
+            const float fb = __fmul_rn(r, a.bins_per_r);
+            if (fb < (float)a.nbins) atomicAdd(&s_h[(uint32_t)fb], 1u);
+        }
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < a.nbins; b += blockDim.x)
+        if (s_h[b]) atomicAdd(&hist[b], (unsigned long long)s_h[b]);
+}
+
 // ------------------------------------------------ parity primitives
 __global__ void k_eval(int op, uint32_t n, const void* in0, const void* in1, uint32_t param,
                        void* out) {

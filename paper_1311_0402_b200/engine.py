@@ -357,6 +357,28 @@ class Engine:
                     kbt=np.array([recs[i].kbt for i in range(k)]),
                     momentum=np.array([tuple(recs[i].momentum) for i in range(k)]).reshape(k, 3))
 
+    # ------------------------------------------- validation observables
+    def profile_reset(self, nbins: int = 50, bin_axis: int = 2, vel_axis: int = 0):
+        """velocity_profile: start accumulating slab averages."""
+        self._check(lib().dpdb_profile_reset(self.h, int(nbins), int(bin_axis), int(vel_axis)))
+        self._prof_nbins = int(nbins)
+
+    def profile_sample(self):
+        self._check(lib().dpdb_profile_sample(self.h))
+
+    def profile(self):
+        """(sum of velocities, counts, samples) per slab since profile_reset."""
+        nb = self._prof_nbins
+        sv, cnt, ns = np.zeros(nb), np.zeros(nb, np.uint64), C.c_int64()
+        self._check(lib().dpdb_profile_get(self.h, ptr(sv), ptr(cnt), C.byref(ns)))
+        return sv, cnt, ns.value
+
+    def rdf_counts(self, nbins: int, rmax: float):
+        """Pair-distance histogram (every pair once) of the current table."""
+        h = np.zeros(int(nbins), np.uint64)
+        self._check(lib().dpdb_rdf(self.h, int(nbins), float(rmax), ptr(h)))
+        return h
+
     def step_timed(self, nsteps: int, stages: bool = False):
         ms = C.c_double()
         st = np.zeros(6) if stages else None
