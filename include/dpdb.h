@@ -119,6 +119,16 @@ int dpdb_download(dpdb_ctx* ctx, double* x, double* y, double* z, double* vx, do
                   uint8_t* species, uint32_t* signature);
 int dpdb_size(const dpdb_ctx* ctx, size_t* n);
 /* Harmonic bonds (BondTopology, inc/core.hpp:70-81): K (r - r0) along the bond */
+/* init_random on the device: n particles uniform in the box,
+ * Maxwell-Boltzmann velocities at kbt with zero net momentum, counter-based
+ * draws tea_hash(16, seed, c) (bit-exact with the oracle's init_fluid when
+ * n_chains = 0).  The first n_chains * chain_len particles form chains (random
+ * walks with step r0, species chain_species[b] per bead, molecule = chain + 1,
+ * harmonic bonds of stiffness bond_k and rest length r0 between neighbours);
+ * the rest are solvent of species solvent_species.  Tags 1..n. */
+int dpdb_init_random(dpdb_ctx* ctx, size_t n, double kbt, uint32_t seed, uint32_t n_chains,
+                     uint32_t chain_len, const uint8_t* chain_species, uint8_t solvent_species,
+                     double r0, double bond_k);
 int dpdb_set_bonds(dpdb_ctx* ctx, size_t nb, const uint32_t* tag_i, const uint32_t* tag_j,
                    const double* k, const double* r0);
 

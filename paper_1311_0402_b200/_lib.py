@@ -89,6 +89,8 @@ SYMBOLS = {
     "dpdb_step": (C.c_int, [C.c_void_p, C.c_int64]),
     "dpdb_thermo_get": (C.c_int, [C.c_void_p, C.POINTER(Thermo)]),
     "dpdb_step_thermo": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(Thermo)]),
+    "dpdb_init_random": (C.c_int, [C.c_void_p, C.c_size_t, C.c_double, C.c_uint32, C.c_uint32,
+                                    C.c_uint32, C.c_void_p, C.c_uint8, C.c_double, C.c_double]),
     "dpdb_profile_reset": (C.c_int, [C.c_void_p, C.c_uint32, C.c_int32, C.c_int32]),
     "dpdb_profile_sample": (C.c_int, [C.c_void_p]),
     "dpdb_profile_get": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]),

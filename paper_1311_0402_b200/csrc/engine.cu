@@ -941,6 +941,78 @@ int dpdb_upload(dpdb_ctx* ctx, size_t n, const double* x, const double* y, const
     return 0;
 }
 
+int dpdb_init_random(dpdb_ctx* ctx, size_t n, double kbt, uint32_t seed, uint32_t n_chains,
+                     uint32_t chain_len, const uint8_t* chain_species, uint8_t solvent_species,
+                     double r0, double bond_k) {
+    TRY(require_ctx(ctx));
+    // init_random validation
+    if (n == 0) return fail(ctx, DPDB_ECONFIG, "init_random: empty system (round(rho V) = 0)");
+    if (n > ctx->cap) return fail(ctx, DPDB_ECONFIG, "init_random: n exceeds context capacity");
+    if (n > 0x0FFFFFFFu / 6) return fail(ctx, DPDB_ECONFIG, "init_random: too many particles for the draw counter");
+    if (!(kbt >= 0)) return fail(ctx, DPDB_ECONFIG, "init_random: kbt must be >= 0");
+    if (n_chains && (chain_len < 2 || chain_len > 32 || !chain_species))
+        return fail(ctx, DPDB_ECONFIG, "init_random: chains of 2..32 beads with a species per bead");
+    if ((size_t)n_chains * chain_len > n) return fail(ctx, DPDB_ECONFIG, "init_random: chains exceed n");
+    for (int k = 0; k < 3; ++k)
+        if (n_chains && r0 * (chain_len - 1) >= ctx->box.hi[k] - ctx->box.lo[k] && !ctx->box.periodic[k])
+            return fail(ctx, DPDB_ECONFIG, "init_random: chain longer than the box");
+    const uint32_t ns = (uint32_t)ctx->params.n_species;
+    if (solvent_species >= ns) return fail(ctx, DPDB_ECONFIG, "init_random: species index out of range");
+    for (uint32_t b = 0; n_chains && b < chain_len; ++b)
+        if (chain_species[b] >= ns) return fail(ctx, DPDB_ECONFIG, "init_random: species index out of range");
+    CK(cudaSetDevice(ctx->device));
+    dpdb::InitArgs a{};
+    for (int k = 0; k < 3; ++k) {
+        a.x[k] = ctx->x[k];
+        a.v[k] = ctx->v[k];
+        a.lo[k] = ctx->box.lo[k];
+        a.hi[k] = ctx->box.hi[k];
+        a.periodic[k] = ctx->box.periodic[k];
+        CK(cudaMemsetAsync(ctx->f[k], 0, ctx->n_pad * 4, ctx->stream));
+    }
+    a.tag = ctx->tag;
+    a.sp = ctx->sp;
+    a.mol = n_chains ? ctx->mol : nullptr;
+    a.sk = std::sqrt(kbt);
+    a.seed = seed;
+    a.n = (uint32_t)n;
+    a.n_chains = n_chains;
+    a.chain_len = n_chains ? chain_len : 1;
+    for (uint32_t b = 0; n_chains && b < chain_len; ++b) a.chain_sp[b] = chain_species[b];
+    a.solvent_sp = solvent_species;
+    a.r0 = r0;
+    CK(cudaMemsetAsync(ctx->sp, 0, ctx->n_pad, ctx->stream));
+    dpdb::k_init_particles<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(a);
+    CKL();
+    if (n_chains) {
+        dpdb::k_init_chains<<<(n_chains + 127) / 128, 128, 0, ctx->stream>>>(a);
+        CKL();
+    }
+    dpdb::k_init_mean<<<1, 32, 0, ctx->stream>>>(a, ctx->red_out);
+    dpdb::k_init_subtract<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(a, ctx->red_out);
+    CKL();
+    ctx->n = n;
+    ctx->has_mol = n_chains > 0;
+    ctx->have_sorted = ctx->have_table = false;
+    ctx->step = 0;
+    if (n_chains) {  // bonds along each chain (BondTopology)
+        std::vector<uint32_t> ti, tj;
+        std::vector<double> kk, rr;
+        for (uint32_t c = 0; c < n_chains; ++c)
+            for (uint32_t b = 0; b + 1 < chain_len; ++b) {
+                const uint32_t t = c * chain_len + b + 1;  // tag = index + 1
+                ti.push_back(t);
+                tj.push_back(t + 1);
+                kk.push_back(bond_k);
+                rr.push_back(r0);
+            }
+        TRY(dpdb_set_bonds(ctx, ti.size(), ti.data(), tj.data(), kk.data(), rr.data()));
+    } else {
+        TRY(refresh_bond_index(ctx));
+    }
+    return check_device(ctx);
+}
+
 int dpdb_upload_forces(dpdb_ctx* ctx, const double* fx, const double* fy, const double* fz) {
     TRY(require_ctx(ctx));
     const double* fs[3] = {fx, fy, fz};

@@ -1225,6 +1225,107 @@ __global__ void k_mean_from_sum(double* sum, double inv_n) {
     if (threadIdx.x < 3) sum[4 + threadIdx.x] = sum[threadIdx.x] * inv_n;
 }
 
+// ------------------------------------------------------ init_random
+// init_random (restated, the reference's init.cpp is not
+// shipped) as counter-based draws, so every particle is independent: draw c of
+// stream `seed` is tea_hash(16, seed, c).  Particle i: position component k from
+// draw 6i + k (uniform in [lo, hi)), velocity component k = sqrt(kT) *
+// gaussian(draw 6i + 3 + k) -- bit-exact with the oracle's init_fluid.  Chains
+// come first (chain c = particles [c L, c L + L)): bead 0 is placed like a
+// solvent particle, bead b > 0 at bead b-1 + r0 * u with the unit vector u
+// from draws 6i (cos theta = 2 u - 1) and 6i + 1 (phi = 2 pi u), wrapped
+// periodically -- the SPEC's random walk with step r0.
+struct InitArgs {
+    double* x[3];
+    double* v[3];
+    uint32_t* tag;
+    uint8_t* sp;
+    uint32_t* mol;
+    double lo[3], hi[3];
+    int periodic[3];
+    double sk;  // sqrt(kT)
+    uint32_t seed, n, n_chains, chain_len;
+    uint8_t chain_sp[32];
+    uint8_t solvent_sp;
+    double r0;
+};
+
+__device__ __forceinline__ uint2 tea16_draw(uint32_t seed, uint32_t c) {
+    uint32_t a = seed, b = c;
+    tea_rounds(16, a, b);
+    return make_uint2(a, b);
+}
+
+__global__ void __launch_bounds__(256) k_init_particles(InitArgs a) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    const uint32_t nb = a.n_chains * a.chain_len;
+    const bool bead = i < nb;
+    const uint32_t b = bead ? i % a.chain_len : 0u;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        if (b == 0) {
+            const uint2 h = tea16_draw(a.seed, 6u * i + (uint32_t)k);
+            const double L = __dsub_rn(a.hi[k], a.lo[k]);
+            double p = __dadd_rn(a.lo[k], __dmul_rn(L, (double)h.x * 0x1p-32));
+            if (p >= a.hi[k]) p = a.lo[k];
+            a.x[k][i] = p;
+        }
+        const uint2 g = tea16_draw(a.seed, 6u * i + 3u + (uint32_t)k);
+        a.v[k][i] = __dmul_rn(a.sk, gaussian64(g.x, g.y));
+    }
+    a.tag[i] = i + 1u;
+    a.sp[i] = bead ? a.chain_sp[b] : a.solvent_sp;
+    if (a.mol) a.mol[i] = bead ? i / a.chain_len + 1u : 0u;
+}
+
+// one thread per chain: the random walk of beads 1..L-1
+__global__ void __launch_bounds__(128) k_init_chains(InitArgs a) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= a.n_chains) return;
+    uint32_t i = c * a.chain_len;
+    double p[3] = {a.x[0][i], a.x[1][i], a.x[2][i]};
+    for (uint32_t b = 1; b < a.chain_len; ++b) {
+        ++i;
+        const uint2 h0 = tea16_draw(a.seed, 6u * i), h1 = tea16_draw(a.seed, 6u * i + 1u);
+        const double ct = __dsub_rn(__dmul_rn(2.0, (double)h0.x * 0x1p-32), 1.0);
+        const double st = sqrt(fmax(__dsub_rn(1.0, __dmul_rn(ct, ct)), 0.0));
+        const double ph = __dmul_rn(6.283185307179586, (double)h1.x * 0x1p-32);
+        const double u[3] = {__dmul_rn(st, cos(ph)), __dmul_rn(st, sin(ph)), ct};
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            double q = __dadd_rn(p[k], __dmul_rn(a.r0, u[k]));
+            const double L = __dsub_rn(a.hi[k], a.lo[k]);
+            if (a.periodic[k]) {
+                if (q < a.lo[k]) q = __dadd_rn(q, L);
+                else if (q >= a.hi[k]) q = __dsub_rn(q, L);
+                if (q >= a.hi[k] || q < a.lo[k]) q = a.lo[k];
+            } else {  // closed axis: reflect back inside
+                if (q < a.lo[k]) q = __dsub_rn(__dmul_rn(2.0, a.lo[k]), q);
+                if (q >= a.hi[k]) q = nextafter(a.hi[k], a.lo[k]);
+            }
+            p[k] = q;
+            a.x[k][i] = q;
+        }
+    }
+}
+
+// zero net momentum: the mean of each component summed in index order
+// by one thread (the oracle's sequential sum, bit for bit), then subtracted
+__global__ void k_init_mean(InitArgs a, double* mean) {
+    const int k = threadIdx.x;
+    if (k >= 3) return;
+    double m = 0.0;
+    for (uint32_t i = 0; i < a.n; ++i) m = __dadd_rn(m, a.v[k][i]);
+    mean[k] = m / (double)a.n;
+}
+__global__ void __launch_bounds__(256) k_init_subtract(InitArgs a, const double* mean) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) a.v[k][i] = __dsub_rn(a.v[k][i], mean[k]);
+}
+
 // ------------------------------------------------ validation observables
 // velocity_profile: per-bin sums of the drive-axis velocity and
 // particle counts along the profile axis.  Velocities are accumulated as

@@ -236,6 +236,18 @@ class Engine:
                                       *[ptr(a) for a in store.veloc], ptr(store.tag),
                                       ptr(store.species), ptr(store.molecule)))
 
+    def init_random(self, n: int, kbt: float = 1.0, seed: int = 1, n_chains: int = 0,
+                    chain_species=(), solvent_species: int = 0, r0: float = 0.38,
+                    bond_k: float = 80.0):
+        """init_random on the device: uniform positions,
+        Maxwell-Boltzmann velocities with zero net momentum, optional chains
+        (random walks with step r0, harmonic bonds k, r0) ahead of the solvent."""
+        cs = np.ascontiguousarray(np.asarray(chain_species, np.uint8))
+        self._keep = None
+        self._check(lib().dpdb_init_random(self.h, int(n), float(kbt), int(seed), int(n_chains),
+                                           int(len(cs)), ptr(cs) if len(cs) else None,
+                                           int(solvent_species), float(r0), float(bond_k)))
+
     def upload_forces(self, fx, fy, fz):
         f = [np.ascontiguousarray(a, np.float64) for a in (fx, fy, fz)]
         self._check(lib().dpdb_upload_forces(self.h, *[ptr(a) for a in f]))
