@@ -164,6 +164,13 @@ int dpdb_verlet_phase2(dpdb_ctx* ctx);
 /* ------------------------------------------------- device-resident path */
 /* Alg. 1 setup: reorder, cell list, build, signatures, forces(step 0) */
 int dpdb_setup(dpdb_ctx* ctx);
+/* restart: setup as at step `step` -- reorder, neighbor build and,
+ * unless keep_forces, forces with step_mix(seed, step).  A restart uploads the
+ * saved forces (dpdb_upload_forces) and keeps them: f(n) was evaluated with the
+ * half-step velocity, so it is state, not recomputable from v(n).  A state saved
+ * after dpdb_step at a rebuild step (step % rebuild_every == 0) then continues
+ * bitwise like the uninterrupted run. */
+int dpdb_setup_at(dpdb_ctx* ctx, int64_t step, int32_t keep_forces);
 /* nsteps of Alg. 1's main loop; rebuild every rebuild_every */
 int dpdb_step(dpdb_ctx* ctx, int64_t nsteps);
 int dpdb_thermo_get(dpdb_ctx* ctx, dpdb_thermo* out);

@@ -87,6 +87,7 @@ SYMBOLS = {
     "dpdb_verlet_phase2": (C.c_int, [C.c_void_p]),
     "dpdb_setup": (C.c_int, [C.c_void_p]),
     "dpdb_step": (C.c_int, [C.c_void_p, C.c_int64]),
+    "dpdb_setup_at": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32]),
     "dpdb_thermo_get": (C.c_int, [C.c_void_p, C.POINTER(Thermo)]),
     "dpdb_step_thermo": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(Thermo)]),
     "dpdb_init_random": (C.c_int, [C.c_void_p, C.c_size_t, C.c_double, C.c_uint32, C.c_uint32,

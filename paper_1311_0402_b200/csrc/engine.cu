@@ -1361,13 +1361,16 @@ int dpdb_verlet_phase2(dpdb_ctx* ctx) {
     return check_device(ctx);
 }
 
-int dpdb_setup(dpdb_ctx* ctx) {
+int dpdb_setup(dpdb_ctx* ctx) { return dpdb_setup_at(ctx, 0, 0); }
+
+int dpdb_setup_at(dpdb_ctx* ctx, int64_t step, int32_t keep_forces) {
     TRY(require_ctx(ctx));
     CK(cudaSetDevice(ctx->device));
-    ctx->step = 0;
-    TRY(do_reorder_all(ctx, false));
+    if (step < 0) return fail(ctx, DPDB_ECONFIG, "setup: step must be >= 0");
+    ctx->step = step;
+    TRY(do_reorder_all(ctx, keep_forces != 0));  // uploaded forces travel with the reorder
     TRY(do_build(ctx, true));
-    TRY(do_forces(ctx, 0));
+    if (!keep_forces) TRY(do_forces(ctx, (uint32_t)step));
     return check_device(ctx);
 }
 

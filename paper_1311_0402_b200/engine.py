@@ -355,6 +355,11 @@ class Engine:
     def setup(self):
         self._check(lib().dpdb_setup(self.h))
 
+    def setup_at(self, step: int, keep_forces: bool = False):
+        """Restart entry (S:680-683): setup with the step counter at `step`;
+        keep_forces keeps forces uploaded with upload_forces (restart state)."""
+        self._check(lib().dpdb_setup_at(self.h, int(step), int(bool(keep_forces))))
+
     def step(self, nsteps: int = 1):
         self._check(lib().dpdb_step(self.h, int(nsteps)))
 
