@@ -156,6 +156,7 @@ struct RunConfig {
     std::uint32_t seed = 1;
     std::uint32_t max_neighbors = 128;
     int sub_bits = 2;
+    int wall_mode = 0;  // 0 specular bounce-forward, 1 bounce-back
     dpdb_run c() const {
         dpdb_run r{};
         r.rebuild_every = rebuild_every;
@@ -166,6 +167,7 @@ struct RunConfig {
         r.seed = seed;
         r.max_neighbors = max_neighbors;
         r.sub_bits = sub_bits;
+        r.wall_mode = wall_mode;
         return r;
     }
 };

@@ -71,6 +71,8 @@ typedef struct {
     uint32_t seed;              /* default 1 */
     uint32_t max_neighbors;     /* default 128, multiple of 32, <= 4096 */
     int32_t sub_bits;           /* default 2 (inc/cell_grid.hpp:30) */
+    int32_t wall_mode;          /* walls: 0 specular "bounce-forward" (default),
+                                   1 bounce-back (every velocity component reversed) */
 } dpdb_run;
 
 /* thermo line */

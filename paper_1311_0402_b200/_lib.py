@@ -37,7 +37,7 @@ class Params(C.Structure):
 class Run(C.Structure):
     _fields_ = [("rebuild_every", C.c_int32), ("skin", C.c_double), ("body_force", C.c_double),
                 ("drive_axis", C.c_int32), ("partition_axis", C.c_int32), ("seed", C.c_uint32),
-                ("max_neighbors", C.c_uint32), ("sub_bits", C.c_int32)]
+                ("max_neighbors", C.c_uint32), ("sub_bits", C.c_int32), ("wall_mode", C.c_int32)]
 
 
 class Thermo(C.Structure):

@@ -232,6 +232,7 @@ dpdb::BoundaryArgs boundary(const dpdb_ctx* ctx) {
         b.periodic[k] = ctx->box.periodic[k];
         b.wall[k] = ctx->box.wall[k];
     }
+    b.bounce_back = ctx->run.wall_mode == 1;
     return b;
 }
 
@@ -704,6 +705,8 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         return fail(nullptr, DPDB_ECONFIG, "capacity: at most 2^26 particles per device context");
     if (run->max_neighbors == 0 || run->max_neighbors % 32 || run->max_neighbors > 4096)
         return fail(nullptr, DPDB_ECONFIG, "run: max_neighbors must be a multiple of 32 in [32, 4096]");
+    if (run->wall_mode != 0 && run->wall_mode != 1)
+        return fail(nullptr, DPDB_ECONFIG, "run: wall_mode must be 0 (specular) or 1 (bounce-back)");
     if (run->drive_axis < 0 || run->drive_axis > 2 || run->partition_axis < 0 || run->partition_axis > 2)
         return fail(nullptr, DPDB_ECONFIG, "run: axes must be 0, 1 or 2");
     ctx = new dpdb_ctx();

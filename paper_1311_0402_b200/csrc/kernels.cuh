@@ -95,11 +95,15 @@ __device__ __forceinline__ bool sort_key_of(const DevGrid& g, double x, double y
 struct BoundaryArgs {
     double lo[3], hi[3], L[3];
     int periodic[3], wall[3];
+    int bounce_back;  // walls reverse the whole velocity (else the normal component)
 };
 
-// periodic wrap right after the position update, specular
-// walls; returns false if the particle is still outside (escaped)
-__device__ __forceinline__ bool apply_boundary(const BoundaryArgs& b, int k, double& x, double& v) {
+// periodic wrap right after the position update, walls
+// mirror the position and reverse the normal velocity (specular; the
+// bounce-back switch reverses the other components in integrate_particle);
+// returns false if the particle is still outside (escaped)
+__device__ __forceinline__ bool apply_boundary(const BoundaryArgs& b, int k, double& x, double& v,
+                                               bool& hit_wall) {
     if (b.periodic[k]) {
         if (x < b.lo[k]) {
             x = __dadd_rn(x, b.L[k]);
@@ -114,10 +118,12 @@ __device__ __forceinline__ bool apply_boundary(const BoundaryArgs& b, int k, dou
         if (x >= b.hi[k]) {
             x = __dsub_rn(__dmul_rn(2.0, b.hi[k]), x);
             v = -v;
+            hit_wall = true;
             if (x >= b.hi[k]) x = nextafter(b.hi[k], b.lo[k]);
         } else if (x < b.lo[k]) {
             x = __dsub_rn(__dmul_rn(2.0, b.lo[k]), x);
             v = -v;
+            hit_wall = true;
             if (x >= b.hi[k]) x = nextafter(b.hi[k], b.lo[k]);
         }
         return x >= b.lo[k] && x < b.hi[k];
@@ -179,6 +185,7 @@ __device__ __forceinline__ void integrate_particle(const IntegrateArgs& a, uint3
                                                    float4* vel4, double vfull[3]) {
     double xs[3], vs[3];
     bool ok = true;
+    uint32_t walls = 0;  // axes whose wall reflected this particle
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         double v = vin[k];
@@ -191,16 +198,24 @@ __device__ __forceinline__ void integrate_particle(const IntegrateArgs& a, uint3
         double x = xin[k];
         if (PHASE1) {
             x = __dadd_rn(x, __dmul_rn(a.dt, v));
+            bool hit = false;
             if (!(isfinite(x) && isfinite(v)))
                 ok = false;
-            else if (!apply_boundary(a.bnd, k, x, v))
+            else if (!apply_boundary(a.bnd, k, x, v, hit))
                 ok = false;
+            walls |= (uint32_t)hit << k;
             a.x[k][i] = x;
         }
-        if (PHASE2 || PHASE1) a.v[k][i] = v;
         xs[k] = x;
         vs[k] = v;
     }
+    if (PHASE1 && walls && a.bnd.bounce_back)  // bounce-back: the tangential components too
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            if (!(walls >> k & 1u)) vs[k] = -vs[k];
+    if (PHASE2 || PHASE1)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) a.v[k][i] = vs[k];
     if (!ok) raise_err(a.err, DPDB_EPHYSICS, EW_NONFINITE, tag, 0);
     if (KEYS) {
         uint32_t key = 0xFFFFFFFFu;

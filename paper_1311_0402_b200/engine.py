@@ -94,12 +94,14 @@ class RunConfig:
     seed: int = 1
     max_neighbors: int = 128
     sub_bits: int = 2
+    wall_mode: int = 0  # 0 specular (default), 1 bounce-back (S:525 design switch)
 
     def _c(self):
         r = Run()
         r.rebuild_every, r.skin, r.body_force = self.rebuild_every, self.skin, self.body_force
         r.drive_axis, r.partition_axis, r.seed = self.drive_axis, self.partition_axis, self.seed
         r.max_neighbors, r.sub_bits = self.max_neighbors, self.sub_bits
+        r.wall_mode = self.wall_mode
         return r
 
 

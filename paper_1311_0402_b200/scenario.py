@@ -15,7 +15,8 @@ whitespace separated.  Species-pair overrides are `a.X.Y = v` / `gamma.X.Y = v`
   [fluid]   density* or n*, kbt*, seed (1), species (S)
   [pair]    a*, sigma* or gamma*, r_c (1), s (1), a.X.Y, gamma.X.Y
   [run]     dt*, steps*, rebuild_every (10), skin (0.3), body_force (0),
-            drive_axis (0), partition_axis (2), max_neighbors (128)
+            drive_axis (0), partition_axis (2), max_neighbors (128),
+            wall_mode (specular | bounce_back)
   [chains]  fraction*, sequence*, r0 (0.38), k (80), solvent (first species)
   [profile] bins (50), axis (2), every (100), start (0)
 (* required; chains/profile sections optional)
@@ -35,7 +36,7 @@ _KEYS = {
     "fluid": {"density", "n", "kbt", "seed", "species"},
     "pair": {"a", "sigma", "gamma", "r_c", "s"},
     "run": {"dt", "steps", "rebuild_every", "skin", "body_force", "drive_axis", "partition_axis",
-            "max_neighbors"},
+            "max_neighbors", "wall_mode"},
     "chains": {"fraction", "sequence", "r0", "k", "solvent"},
     "profile": {"bins", "axis", "every", "start"},
 }
@@ -182,7 +183,10 @@ def parse_text(text: str, source: str = "<string>") -> Scenario:
                     drive_axis=_num(r.get("drive_axis", "0"), "run.drive_axis", int),
                     partition_axis=_num(r.get("partition_axis", "2"), "run.partition_axis", int),
                     seed=_num(f.get("seed", "1"), "fluid.seed", int),
-                    max_neighbors=_num(r.get("max_neighbors", "128"), "run.max_neighbors", int))
+                    max_neighbors=_num(r.get("max_neighbors", "128"), "run.max_neighbors", int),
+                    wall_mode={"specular": 0, "bounce_back": 1}.get(r.get("wall_mode", "specular"), -1))
+    if run.wall_mode < 0:
+        raise DPDError(1, "config: run.wall_mode must be specular or bounce_back")
     if run.rebuild_every < 1 or run.skin < 0:
         raise DPDError(1, "config: run.rebuild_every >= 1 and run.skin >= 0")
     steps = _num(r["steps"], "run.steps", int)

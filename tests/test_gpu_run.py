@@ -212,3 +212,37 @@ def test_step_thermo_records(monkeypatch, fuse):
         assert np.array_equal(u, w)
     rec2 = b.step_thermo(3)  # a second call continues the step count
     assert list(rec2["step"]) == [12, 13, 14]
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_closed_box_walls(mode):
+    """walls on every axis, ideal gas with a = gamma = sigma = 0:
+    no particle ever outside the box and kinetic energy conserved exactly
+    (reflections only flip velocity signs), for the specular bounce-forward
+    (default) and the bounce-back switch; bounce-back reverses the whole
+    velocity of a particle that hits a wall."""
+    L = (6.0, 5.0, 4.0)
+    box, obox, st = _sys.fluid(L, 3.0, (0, 0, 0), seed=19, wall=(1, 1, 1))
+    st = list(st)
+    for k in range(3):
+        st[3 + k] = st[3 + k] * 20.0  # fast particles: many wall hits per step
+    p = dpd.PairParams.make(1, 0.0, 0.0, 0.0, 1.0, 1.0, 0.01)
+    e = _sys.engine(box, st, params=p, run=dpd.RunConfig(wall_mode=mode))
+    e.setup()
+    ke0 = sum(float(np.dot(v, v)) for v in e.download().veloc)
+    for _ in range(20):
+        e.step(5)
+        s = e.download()
+        X = np.stack(s.coord, 1)
+        assert np.all(X >= 0) and np.all(X < np.array(L))
+    assert sum(float(np.dot(v, v)) for v in s.veloc) == pytest.approx(ke0, rel=1e-12)
+    # one particle crossing hi by eps
+    one = dpd.Engine(dpd.SimBox((0.0, 0.0, 0.0), L, (False,) * 3, (True,) * 3), p,
+                     dpd.RunConfig(wall_mode=mode), capacity=1)
+    one.upload(dpd.ParticleStore.from_arrays([5.99], [2.0], [2.0], [2.0], [0.5], [-0.25], [1]))
+    one.setup()
+    one.step(1)
+    s = one.download()
+    assert s.coord[0][0] == pytest.approx(6.0 - 0.01, abs=1e-12)
+    v = [s.veloc[k][0] for k in range(3)]
+    assert v == ([-2.0, 0.5, -0.25] if mode == 0 else [-2.0, -0.5, 0.25])
