@@ -103,9 +103,9 @@ __device__ __forceinline__ float weight_pow_f(float w, float s, int mode) {
     return w > 0.f ? exp2f(s * __log2f(w)) : 0.f;
 }
 
-constexpr int FORCE_WARPS = 8;   // warps per CTA
-constexpr int FORCE_TILES = 16;  // 32-row tiles per CTA block: B = 512 particles
-constexpr int FORCE_BLOCK = 32 * FORCE_TILES;
+constexpr int FORCE_WARPS = DPDB_FORCE_WARPS;  // warps per CTA (kernels.cuh)
+constexpr int FORCE_TILES = 2 * FORCE_WARPS;    // 32-row tiles per CTA block
+constexpr int FORCE_BLOCK = 32 * FORCE_TILES;   // B particles per block (== RB_BLOCK)
 constexpr int FQ = 64;  // per-warp pair queue (slots)
 // Forces are accumulated as 2^-18 fixed-point int32 (|F| < 8192 per particle,
 // resolution 3.8e-6): integer sums commute, so the result does not depend on
@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(ForceArgs a) {
 // rotating register pipeline.  The queue (160 slots) is drained once per
 // group, in whole batches of 32.
 //
-// Each warp takes tiles (w, 15 - w) of the block: in-block pairs are taken by
+// Each warp takes tiles (w, FORCE_TILES - 1 - w) of the block: in-block pairs are taken by
 // the lower index, so early tiles carry more pairs; pairing them with late
 // tiles evens out the work before the block's final barrier.
 #ifndef DPDB_FW_UNCOND
@@ -334,7 +334,9 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(ForceArgs a) {
 #endif
 constexpr bool FW_UNCOND = DPDB_FW_UNCOND;
 #ifndef FW_MINB
-#define FW_MINB 4  // resident CTAs per SM the register allocation must allow (A/B: 1, 3, 4 -> 4 best)
+// resident CTAs per SM the register allocation must allow: 32 warps / SM
+// (64 registers; A/B at 8 warps per CTA: 1, 3, 4 CTAs -> 4 best, 5 spills)
+#define FW_MINB (32 / DPDB_FORCE_WARPS)
 #endif  // A/B switch: unpredicated phase-A loads
 #ifndef DPDB_FW_PREFETCH
 #define DPDB_FW_PREFETCH 0
