@@ -14,8 +14,8 @@ from paper_1311_0402_b200.observables import (analytic_transient_profile, estima
                                               velocity_profile)
 
 g = 0.055
-for seed in (7, 8, 9):
-    e = T.poiseuille_engine((12.0, 8.0, 8.0), 6.0, 0.0, 4.5, 0.5, 0.001, g, seed)
+for seed in (7, 8, 9, 10):
+    e = T.poiseuille_engine((12.0, 32.0, 8.0), 6.0, 0.0, 4.5, 0.5, 0.001, g, seed)
     e.step(60000)
     e.profile_reset(32, 2, 0)
     for _ in range(600):
