@@ -1615,12 +1615,12 @@ int dpdb_thermo_get(dpdb_ctx* ctx, dpdb_thermo* out) {
     if (!ctx->n) return fail(ctx, DPDB_EPHYSICS, "temperature of an empty system");
     dpdb::k_sum3<<<RED_BLOCKS, 256, 0, ctx->stream>>>(ctx->v[0], ctx->v[1], ctx->v[2], nullptr,
                                                       (uint32_t)ctx->n, ctx->red);
-    dpdb::k_sum_partials<<<1, 32, 0, ctx->stream>>>(ctx->red, RED_BLOCKS, ctx->red_out);
+    dpdb::k_sum_partials<<<1, 256, 0, ctx->stream>>>(ctx->red, RED_BLOCKS, ctx->red_out);
     dpdb::k_mean_from_sum<<<1, 32, 0, ctx->stream>>>(ctx->red_out, 1.0 / (double)ctx->n);
     // second pass around the device-resident mean; one read-back for both
     dpdb::k_sum3<<<RED_BLOCKS, 256, 0, ctx->stream>>>(ctx->v[0], ctx->v[1], ctx->v[2],
                                                       ctx->red_out + 4, (uint32_t)ctx->n, ctx->red);
-    dpdb::k_sum_partials<<<1, 32, 0, ctx->stream>>>(ctx->red, RED_BLOCKS, ctx->red_out + 8);
+    dpdb::k_sum_partials<<<1, 256, 0, ctx->stream>>>(ctx->red, RED_BLOCKS, ctx->red_out + 8);
     double r[16];
     CK(cudaMemcpyAsync(r, ctx->red_out, sizeof r, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));

@@ -1234,12 +1234,14 @@ __global__ void __launch_bounds__(256) k_sum3(const double* __restrict__ a0,
     if (threadIdx.x < 4) partial[blockIdx.x * 4 + threadIdx.x] = s[threadIdx.x][0];
 }
 
-__global__ void k_sum_partials(const double* partial, int nblocks, double* out) {
-    if (threadIdx.x != 0) return;
+// fixed-order sum of the block partials: thread t adds blocks t, t + 256, ...
+// then block_sum4 (deterministic for a given nblocks); launch with 256 threads
+__global__ void __launch_bounds__(256) k_sum_partials(const double* partial, int nblocks, double* out) {
     double acc[4] = {0, 0, 0, 0};
-    for (int b = 0; b < nblocks; ++b)
+    for (int b = threadIdx.x; b < nblocks; b += 256)
+#pragma unroll
         for (int q = 0; q < 4; ++q) acc[q] += partial[b * 4 + q];
-    for (int q = 0; q < 4; ++q) out[q] = acc[q];
+    block_sum4<256>(acc, out);
 }
 
 __global__ void k_mean_from_sum(double* sum, double inv_n) {
