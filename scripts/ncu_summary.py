@@ -33,6 +33,8 @@ METRICS = [
     ("L1 hit %", "l1tex__t_sector_hit_rate.pct"),
     ("L2 hit %", "lts__t_sector_hit_rate.pct"),
     ("Avg active threads/warp", "smsp__thread_inst_executed_per_inst_executed.ratio"),
+    ("Global ld useful bytes/sector", "smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.ratio"),
+    ("Global ld L1 sector hit %", "l1tex__t_sector_pipe_lsu_mem_global_op_ld_hit_rate.pct"),
 ]
 
 
@@ -93,6 +95,12 @@ def main(tag):
             for label, m in METRICS:
                 if m in d:
                     md.append(f"| {label} | {d[m]} {d['_units'].get(m, '')} |")
+            try:
+                sec = float(d["l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum"].replace(",", ""))
+                req = float(d["l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum"].replace(",", ""))
+                md.append(f"| Global ld sectors/request | {sec / max(req, 1):.2f} |")
+            except (KeyError, ValueError):
+                pass
             try:
                 rb = float(d["dram__bytes_read.sum"].replace(",", ""))
                 wb = float(d["dram__bytes_write.sum"].replace(",", ""))
