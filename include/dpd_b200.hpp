@@ -34,6 +34,7 @@
 #include <array>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -239,6 +240,37 @@ public:
         ck(dpdb_thermo_get(ctx_, &t));
         return t;
     }
+    // init_random on the device; chains ahead of the solvent
+    void init_random(std::size_t n, double kbt, std::uint32_t seed, std::uint32_t n_chains = 0,
+                     const std::vector<std::uint8_t>& chain_species = {}, std::uint8_t solvent = 0,
+                     double r0 = 0.38, double bond_k = 80.0) {
+        ck(dpdb_init_random(ctx_, n, kbt, seed, n_chains, (std::uint32_t)chain_species.size(),
+                            chain_species.empty() ? nullptr : chain_species.data(), solvent, r0,
+                            bond_k));
+    }
+    // restart entry: setup at `step`, keeping uploaded forces
+    void setup_at(std::int64_t step, bool keep_forces) { ck(dpdb_setup_at(ctx_, step, keep_forces)); }
+    void upload_forces(const ParticleStore& s) {
+        ck(dpdb_upload_forces(ctx_, s.force[0].data(), s.force[1].data(), s.force[2].data()));
+    }
+    // velocity_profile accumulation
+    void profile_reset(std::uint32_t bins, int bin_axis, int vel_axis) {
+        ck(dpdb_profile_reset(ctx_, bins, bin_axis, vel_axis));
+    }
+    void profile_sample() { ck(dpdb_profile_sample(ctx_)); }
+    // per-bin (sum of velocities, count) and the sample count
+    std::int64_t profile(std::vector<double>& sum_v, std::vector<std::uint64_t>& count) {
+        std::int64_t ns = 0;
+        ck(dpdb_profile_get(ctx_, sum_v.data(), count.data(), &ns));
+        return ns;
+    }
+    // pair-distance histogram of the current table (every pair once)
+    std::vector<std::uint64_t> rdf_counts(std::uint32_t bins, double rmax) {
+        std::vector<std::uint64_t> h(bins);
+        ck(dpdb_rdf(ctx_, bins, rmax, h.data()));
+        return h;
+    }
+    std::int64_t current_step() const { return dpdb_current_step(ctx_); }
 
 private:
     dpdb_ctx* ctx_ = nullptr;
@@ -392,6 +424,53 @@ inline double fastpow(double a, double b, int device = 0) {
     double out;
     check(dpdb_eval(device, DPDB_OP_FASTPOW, 1, &a, &b, 0, &out));
     return out;
+}
+
+// ------------------------------------------------ observables and outputs
+// (same definitions as paper_1311_0402_b200/observables.py, io.py)
+
+// estimate_viscosity: least squares u(z) = (g rho / (2 mu)) z (d - z)
+inline double estimate_viscosity(const std::vector<double>& z, const std::vector<double>& u, double g,
+                                 double rho, double d) {
+    double pu = 0, pp = 0;
+    for (std::size_t k = 0; k < z.size(); ++k) {
+        if (!(u[k] == u[k])) continue;  // empty bin (nan)
+        const double phi = z[k] * (d - z[k]);
+        pu += phi * u[k];
+        pp += phi * phi;
+    }
+    return g * rho / (2.0 * (pu / pp));
+}
+
+// analytic_transient_profile (Eq. 9), n_terms terms of the series
+inline double analytic_transient_profile(double z, double t, double F, double d, double nu,
+                                         long n_terms = 200000) {
+    const double pi = 3.14159265358979323846;
+    double u = F * d * d / (8.0 * nu) * (1.0 - (2.0 * z / d) * (2.0 * z / d));
+    for (long n = 0; n < n_terms; ++n) {
+        const double k = 2.0 * n + 1.0;
+        const double term = 4.0 * F * d * d / (nu * pi * pi * pi * k * k * k) * std::cos(k * pi * z / d) *
+                            std::exp(-k * k * pi * pi * nu * t / (d * d));
+        u -= (n % 2 ? -1.0 : 1.0) * term;
+    }
+    return u;
+}
+
+// XYZ frame: count line, comment line, "name x y z" per particle
+inline void write_xyz(std::FILE* f, const ParticleStore& s, const char* comment = "",
+                      const char* names = "SABC") {
+    std::fprintf(f, "%zu\n%s\n", s.n, comment);
+    for (std::size_t i = 0; i < s.n; ++i)
+        std::fprintf(f, "%c %.10g %.10g %.10g\n", names[s.species.empty() ? 0 : s.species[i]],
+                     s.coord[0][i], s.coord[1][i], s.coord[2][i]);
+}
+
+// thermo CSV: step, time, kbt, px, py, pz, n
+inline void write_thermo_csv(std::FILE* f, const std::vector<dpdb_thermo>& rec, double dt) {
+    std::fprintf(f, "step,time,kbt,px,py,pz,n\n");
+    for (const auto& r : rec)
+        std::fprintf(f, "%lld,%.10g,%.17g,%.17g,%.17g,%.17g,%llu\n", (long long)r.step, r.step * dt, r.kbt,
+                     r.momentum[0], r.momentum[1], r.momentum[2], (unsigned long long)r.n);
 }
 
 }  // namespace dpd::b200

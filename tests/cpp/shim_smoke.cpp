@@ -43,6 +43,26 @@ int main() {
         dev.setup();
         dev.step(20);
         const dpdb_thermo th = dev.thermo();
+        // per-step thermo lines, observables, device init (the reference's run() path)
+        const auto lines = dev.step_thermo(10);
+        dev.profile_reset(8, 2, 0);
+        dev.profile_sample();
+        std::vector<double> sv(8);
+        std::vector<std::uint64_t> cnt(8);
+        const std::int64_t ns = dev.profile(sv, cnt);
+        std::uint64_t tot = 0;
+        for (auto c : cnt) tot += c;
+        const auto hist = dev.rdf_counts(13, 1.3);
+        Device dev2(box, params, run, n);
+        dev2.init_random(n, 1.0, 7);
+        dev2.setup();
+        dev2.step(5);
+        if (lines.size() != 10 || lines.back().step != dev.current_step() || ns != 1 || tot != n ||
+            hist[10] == 0 || dev2.current_step() != 5) {
+            std::printf("shim observables wrong\n");
+            return 2;
+        }
+        write_thermo_csv(stdout, {lines.back()}, 0.01);
         std::printf("shim ok n=%zu perm0=%u core_pairs=%zu joined=%d net_force=(%.2e,%.2e,%.2e) kbt=%.4f "
                     "fastlog(2^31)=%.17g\n",
                     n, perm[0], pairs, (int)t.joined, net[0], net[1], net[2], th.kbt,
