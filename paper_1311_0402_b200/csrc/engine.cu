@@ -511,16 +511,36 @@ void force_dispatch_layout(dpdb_ctx* ctx, const dpdb::ForceArgs& a, bool body, i
 }
 
 // Whether the step loop may run the next Verlet pass inside the force kernel:
-// single domain, walk layout with 128-slot rows, no bonds (their forces are
-// added by a separate pass after the pair forces).
+// single domain, walk layout with 128-slot rows (the walk kernel adds the
+// bond forces in its epilogue, so bonds fuse too).
 bool can_fuse(const dpdb_ctx* ctx) {
-    return ctx->walk && ctx->maxn == 128 && !ctx->n_bonds && !ctx->md_valid &&
+    return ctx->walk && ctx->maxn == 128 && !ctx->md_valid &&
            ctx->dims[0] * ctx->dims[1] * ctx->dims[2] == 1 && !ctx->no_fuse;
 }
 
 // fuse (step loop only, can_fuse): FUSE_STREAMS / FUSE_KEYS run phase 2 of
 // this step + phase 1 of the next in the force kernel's epilogue; the forces
 // themselves are then not stored.
+dpdb::BondArgs bond_args(dpdb_ctx* ctx) {
+    dpdb::BondArgs b{};
+    b.boff = ctx->bond_off;
+    b.bpartner = ctx->bond_partner;
+    b.bk = ctx->bond_k;
+    b.br0 = ctx->bond_r0;
+    b.index_of_tag = ctx->index_of_tag;
+    b.pos4 = ctx->pos4;
+    for (int k = 0; k < 3; ++k) {
+        b.f[k] = ctx->f[k];
+        b.periodic[k] = ctx->box.periodic[k];
+    }
+    wrap_lengths(ctx, b.L, b.H);
+    b.err = ctx->err;
+    b.n = (uint32_t)ctx->n;
+    b.max_tag = ctx->max_tag;
+    b.tag_mask = ctx->multi ? 0x0FFFFFFFu : 0xFFFFFFFFu;
+    return b;
+}
+
 // part (bricks, walk layout): -1 every block; 0 the interior blocks (no ghost
 // partner: they can run while the ghost update is in flight); 1 the rest
 int do_forces(dpdb_ctx* ctx, uint32_t step, int fuse = dpdb::FUSE_NONE, bool thermo = false,
@@ -560,6 +580,10 @@ int do_forces(dpdb_ctx* ctx, uint32_t step, int fuse = dpdb::FUSE_NONE, bool the
         a.tg[q] = (float)p.gamma[q];
         a.ts[q] = (float)(ctx->sigma[q] / std::sqrt(p.dt));
     }
+    if (ctx->n_bonds && ctx->walk) {
+        a.has_bonds = 1;
+        a.bd = bond_args(ctx);
+    }
     if (part >= 0) {
         a.blk_sel = ctx->blk_ghost;
         a.sel_val = (uint32_t)part;
@@ -570,29 +594,14 @@ int do_forces(dpdb_ctx* ctx, uint32_t step, int fuse = dpdb::FUSE_NONE, bool the
         a.pos4n = ctx->pos4n;
         a.vel4n = ctx->vel4n;
     }
-    if (ctx->multi || a.smode != 1)
+    if (ctx->multi || a.smode != 1 || a.has_bonds)  // bonds: in the GENERAL epilogue
         force_dispatch_layout<true>(ctx, a, body, fuse);
     else
         force_dispatch_layout<false>(ctx, a, body, fuse);
     CKL();
     ctx->launches[ST_FORCE]++;
-    if (ctx->n_bonds) {
-        dpdb::BondArgs b{};
-        b.boff = ctx->bond_off;
-        b.bpartner = ctx->bond_partner;
-        b.bk = ctx->bond_k;
-        b.br0 = ctx->bond_r0;
-        b.index_of_tag = ctx->index_of_tag;
-        b.pos4 = ctx->pos4;
-        for (int k = 0; k < 3; ++k) {
-            b.f[k] = ctx->f[k];
-            b.periodic[k] = ctx->box.periodic[k];
-        }
-        wrap_lengths(ctx, b.L, b.H);
-        b.err = ctx->err;
-        b.n = (uint32_t)ctx->n;
-        b.max_tag = ctx->max_tag;
-        b.tag_mask = ctx->multi ? 0x0FFFFFFFu : 0xFFFFFFFFu;
+    if (ctx->n_bonds && !ctx->walk) {  // the walk kernel added them in its epilogue
+        dpdb::BondArgs b = bond_args(ctx);
         dpdb::k_bonds<<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(b);
         CKL();
         ctx->launches[ST_FORCE]++;

@@ -39,6 +39,9 @@ struct ForceArgs {
     // boundary split around the ghost update); null = every block
     const uint8_t* blk_sel;
     uint32_t sel_val;
+    // k_force_walk<GENERAL>: harmonic bonds added in the epilogue (else k_bonds runs after)
+    int has_bonds;
+    BondArgs bd;
 };
 
 enum ForceFuse : int { FUSE_NONE = 0, FUSE_STREAMS = 1, FUSE_KEYS = 2 };
@@ -539,6 +542,17 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceA
     constexpr int PER_T = FORCE_BLOCK / (FORCE_WARPS * 32);
     double ex[FUSE ? PER_T : 1][6];
     uint32_t etag[FUSE ? PER_T : 1], esp[FUSE ? PER_T : 1];
+    // bond forces (independent of the pair sums): evaluated before the barrier
+    // too, their dependent tag -> index -> position loads hide behind it
+    // (GENERAL instantiations only: the host dispatches bonded systems there)
+    float bf[PER_T][3];
+    bool bset[PER_T];
+#pragma unroll
+    for (int q = 0; q < PER_T; ++q) {
+        const uint32_t t = threadIdx.x + q * FORCE_WARPS * 32;
+        bset[q] = GENERAL && a.has_bonds && t < bn &&
+                  bond_force(a.bd, b0 + t, bf[q][0], bf[q][1], bf[q][2]);
+    }
     if (FUSE != FUSE_NONE) {
 #pragma unroll
         for (int q = 0; q < PER_T; ++q) {
@@ -573,6 +587,11 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceA
                 fy += g;
             else
                 fz += g;
+        }
+        if (GENERAL && bset[q]) {  // same fp32 adds as k_bonds after the pair kernel
+            fx += bf[q][0];
+            fy += bf[q][1];
+            fz += bf[q][2];
         }
         if (FUSE == FUSE_NONE) {
             a.f[0][i] = fx;

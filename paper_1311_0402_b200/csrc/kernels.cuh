@@ -1153,9 +1153,6 @@ __global__ void k_tile_transpose(uint32_t* entries, uint32_t n_rows_pad, uint32_
         entries[(size_t)(tr + y) * maxn + tc + threadIdx.x] = t[threadIdx.x][y];
 }
 
-#include "force.cuh"
-#include "domain.cuh"
-
 // Harmonic bonds: F = -K (r - r0) e on each endpoint.  Bonds are
 // stored as a static CSR over TAGS (each bond at both endpoints), resolved
 // to current indices through index_of_tag (refreshed at every reorder), and
@@ -1175,15 +1172,16 @@ struct BondArgs {
     uint32_t tag_mask;  // 0x0FFFFFFF when species ride in pos4.w
 };
 
-__global__ void k_bonds(BondArgs a) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= a.n) return;
+// harmonic bond force on particle i (every bond of i, in CSR order); false if
+// the particle has no bonds.  Shared by k_bonds and the pair kernel epilogue.
+__device__ __forceinline__ bool bond_force(const BondArgs& a, uint32_t i, float& fx, float& fy,
+                                           float& fz) {
     const float4 pi = a.pos4[i];
     const uint32_t tag = __float_as_uint(pi.w) & a.tag_mask;
-    if (tag > a.max_tag) return;
+    if (tag > a.max_tag) return false;
     const uint32_t b0 = a.boff[tag], b1 = a.boff[tag + 1];
-    if (b0 == b1) return;
-    float fx = 0.f, fy = 0.f, fz = 0.f;
+    if (b0 == b1) return false;
+    fx = fy = fz = 0.f;
     for (uint32_t b = b0; b < b1; ++b) {
         const uint32_t pt = a.bpartner[b];
         const uint32_t j = a.index_of_tag[pt];
@@ -1202,10 +1200,21 @@ __global__ void k_bonds(BondArgs a) {
         fy += cc * d[1];
         fz += cc * d[2];
     }
+    return true;
+}
+
+__global__ void k_bonds(BondArgs a) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    float fx, fy, fz;
+    if (!bond_force(a, i, fx, fy, fz)) return;
     a.f[0][i] += fx;
     a.f[1][i] += fy;
     a.f[2][i] += fz;
 }
+
+#include "force.cuh"
+#include "domain.cuh"
 
 // --------------------------------------------------- observables
 // deterministic two-level reductions (fixed tree, fixed partial order)

@@ -109,6 +109,41 @@ def test_fused_force_integrate_equals_separate_pass(monkeypatch, case):
         assert np.array_equal(u, w)
 
 
+def test_bonded_pipeline_equals_stagewise_api():
+    """With harmonic bonds the step loop adds the bond forces in the pair
+    kernel's epilogue (and still fuses the Verlet pass); the stage-by-stage
+    ABI adds them with the separate k_bonds pass.  Same trajectory bit for
+    bit (three species, 8-bead chains)."""
+    L = (10.0, 10.0, 10.0)
+    p = dpd.PairParams.make(3, [15, 15, 120, 15, 15, 120, 120, 120, 15], 4.5, 1.0, 1.0, 1.0, 0.01)
+    box = dpd.SimBox((0.0, 0.0, 0.0), L)
+    n, nc, seq = 5000, 60, [2, 2, 2, 1, 1, 2, 2, 2]
+
+    def fresh():
+        e = dpd.Engine(box, p, dpd.RunConfig(), capacity=n)
+        e.init_random(n, 1.0, 9, nc, seq, 0, 0.38, 80.0)
+        return e
+
+    a = fresh()
+    a.setup()
+    a.step(23)
+    b = fresh()
+    b.reorder_particles()
+    b.build_neighbor_table()
+    b.compute_forces(0)
+    for step in range(1, 24):
+        b.verlet_phase1()
+        if step % 10 == 0:
+            b.reorder_particles()
+            b.build_neighbor_table()
+        b.compute_forces(step)
+        b.verlet_phase2()
+    sa, sb = a.download(), b.download()
+    oa, ob = np.argsort(sa.tag), np.argsort(sb.tag)
+    for u, w in zip(sa.coord + sa.veloc + sa.force, sb.coord + sb.veloc + sb.force):
+        assert np.array_equal(u[oa], w[ob])
+
+
 def test_first_step_vs_oracle_driver():
     """Setup + one step against the oracle's Alg. 1 driver.  After one step
     the fp64 positions agree to fp32-force rounding; beyond that trajectories
