@@ -108,6 +108,7 @@ struct dpdb_ctx {
     uint32_t md_moff[27]{}, md_goff[27]{};
     uint32_t md_n_out = 0, md_n_all = 0;
     bool md_in_rebuild = false, md_pending_p2 = false;
+    bool md_integrated = false;  // the next step's Verlet pass already ran in the force epilogue
     std::array<int32_t, 26> md_gcnt{};  // ghosts this brick sends per direction
     std::array<int32_t, 26> md_rcnt{};  // ghosts it receives per direction
     void *md_sbuf{}, *md_rbuf{};         // packed records out / in (device)
@@ -544,7 +545,7 @@ dpdb::BondArgs bond_args(dpdb_ctx* ctx) {
 // part (bricks, walk layout): -1 every block; 0 the interior blocks (no ghost
 // partner: they can run while the ghost update is in flight); 1 the rest
 int do_forces(dpdb_ctx* ctx, uint32_t step, int fuse = dpdb::FUSE_NONE, bool thermo = false,
-              int part = -1) {
+              int part = -1, bool defer_wrap = false) {
     if (!ctx->have_table) return fail(ctx, DPDB_ECONFIG, "compute_forces: neighbor table not built");
     if (!ctx->n) return 0;
     const dpdb_params& p = ctx->params;
@@ -589,7 +590,7 @@ int do_forces(dpdb_ctx* ctx, uint32_t step, int fuse = dpdb::FUSE_NONE, bool the
         a.sel_val = (uint32_t)part;
     }
     if (fuse != dpdb::FUSE_NONE) {
-        a.ia = integrate_args(ctx, false);
+        a.ia = integrate_args(ctx, defer_wrap);
         if (thermo) a.ia.thermo_part = ctx->thermo_part;
         a.pos4n = ctx->pos4n;
         a.vel4n = ctx->vel4n;
