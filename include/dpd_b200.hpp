@@ -473,4 +473,41 @@ inline void write_thermo_csv(std::FILE* f, const std::vector<dpdb_thermo>& rec, 
                      r.momentum[0], r.momentum[1], r.momentum[2], (unsigned long long)r.n);
 }
 
+// minimum_image (src/core.cpp:129-139): half-open on periodic axes
+inline Vec3 minimum_image(Vec3 dr, const SimBox& box) {
+    for (int k = 0; k < 3; ++k) {
+        if (!box.periodic[k]) continue;
+        const double L = box.length(k);
+        double& d = (&dr.x)[k];
+        if (d >= 0.5 * L)
+            d -= L;
+        else if (d < -0.5 * L)
+            d += L;
+    }
+    return dr;
+}
+
+// dump_neighbor_csv (inc/neighbor_table.hpp:57-59): one line per table entry,
+// i_tag, j_tag, distance (fp64 minimum image on the `wrap` axes), partition
+// (core / skin); the store must be the one the table was built from
+inline void dump_neighbor_csv(const NeighborTable& t, const ParticleStore& s, const SimBox& box,
+                              const std::array<bool, 3>& wrap, std::FILE* f) {
+    std::fprintf(f, "i_tag,j_tag,distance,partition\n");
+    SimBox wb = box;
+    wb.periodic = wrap;
+    for (std::uint32_t i = 0; i < t.n_rows; ++i) {
+        for (int part = 0; part < 2; ++part) {
+            const std::uint32_t cnt = part ? t.skin_count[i] : t.core_count[i];
+            for (std::uint32_t k = 0; k < cnt; ++k) {
+                const std::uint32_t j = part ? t.skin_at(i, k) : t.core_at(i, k);
+                Vec3 d{s.coord[0][i] - s.coord[0][j], s.coord[1][i] - s.coord[1][j],
+                       s.coord[2][i] - s.coord[2][j]};
+                d = minimum_image(d, wb);
+                std::fprintf(f, "%u,%u,%.17g,%s\n", s.tag[i], s.tag[j],
+                             std::sqrt(d.x * d.x + d.y * d.y + d.z * d.z), part ? "skin" : "core");
+            }
+        }
+    }
+}
+
 }  // namespace dpd::b200

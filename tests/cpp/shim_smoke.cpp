@@ -31,8 +31,23 @@ int main() {
         Device dev(box, params, run, n);
         const auto perm = reorder_particles(st, dev);
         NeighborTable t = build_neighbor_table(st, dev, run.max_neighbors);
-        std::size_t pairs = 0;
-        for (std::uint32_t i = 0; i < t.n_rows; ++i) pairs += t.core_count[i];
+        std::size_t pairs = 0, entries = 0;
+        for (std::uint32_t i = 0; i < t.n_rows; ++i) {
+            pairs += t.core_count[i];
+            entries += t.core_count[i] + t.skin_count[i];
+        }
+        {  // dump_neighbor_csv (inc/neighbor_table.hpp:57-59): header + one line per entry
+            std::FILE* f = std::tmpfile();
+            dump_neighbor_csv(t, st, box, {true, true, true}, f);
+            std::rewind(f);
+            std::size_t lines = 0;
+            for (int c; (c = std::fgetc(f)) != EOF;) lines += c == '\n';
+            std::fclose(f);
+            if (lines != entries + 1) {
+                std::printf("dump_neighbor_csv: %zu lines for %zu entries\n", lines, entries);
+                return 3;
+            }
+        }
         join_core_skin(t, dev);
         compute_forces(st, dev, 0);
         double net[3] = {0, 0, 0};

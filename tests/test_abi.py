@@ -96,3 +96,25 @@ def test_config_errors_before_device():
     with pytest.raises(dpd.DPDError) as e:
         dpd.radix_sort(*(__import__("numpy").zeros(4, "uint32") for _ in range(2)), 6)
     assert e.value.code == 1
+
+
+def test_shim_minimum_image_examples(tmp_path):
+    """S:55-60 examples through the C++ shim's minimum_image (header-only, no GPU)."""
+    src = tmp_path / "mi.cpp"
+    src.write_text('''#include "dpd_b200.hpp"
+#include <cstdio>
+using namespace dpd::b200;
+int main() {
+    SimBox b;
+    b.hi = {12.0, 8.0, 8.0};
+    b.periodic = {true, true, false};
+    Vec3 z = minimum_image({0, 0, 0}, b), w = minimum_image({7, -4.5, 30}, b);
+    std::printf("%g %g %g %g %g %g\\n", z.x, z.y, z.z, w.x, w.y, w.z);
+    return 0;
+}
+''')
+    exe = tmp_path / "mi"
+    subprocess.run(["g++", "-std=c++17", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)],
+                   check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()
+    assert [float(v) for v in out] == [0, 0, 0, -5, 3.5, 30]  # L_x = 12: 7 -> -5; wall/free axis unchanged
