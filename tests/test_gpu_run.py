@@ -49,13 +49,16 @@ def test_blowup_is_physics_error():
     assert ex.value.code == 2
 
 
-def test_fused_step_equals_stagewise_api():
+@pytest.mark.parametrize("s_exp", [1.0, 0.5])
+def test_fused_step_equals_stagewise_api(s_exp):
     """dpdb_step's fused kernels (phase2+phase1+streams, reorder, build, force)
-    reproduce the stage-by-stage ABI sequence of Alg. 1 bit for bit."""
+    reproduce the stage-by-stage ABI sequence of Alg. 1 bit for bit (s = 0.5:
+    the general weight-exponent path of the walk kernel)."""
     box, obox, st = _sys.fluid((12, 12, 12), 3.0, seed=21)
-    a = _sys.engine(box, st)
+    p = dpd.PairParams.make(1, 25.0, 4.5, 1.0, s_exp, 1.0, 0.01)
+    a = _sys.engine(box, st, params=p)
     a.setup()
-    b = _sys.engine(box, st)
+    b = _sys.engine(box, st, params=p)
     b.reorder_particles()
     b.build_neighbor_table()
     b.compute_forces(0)
@@ -71,7 +74,7 @@ def test_fused_step_equals_stagewise_api():
     assert np.array_equal(sa.tag, sb.tag)
     for u, w in zip(sa.coord + sa.veloc + sa.force, sb.coord + sb.veloc + sb.force):
         assert np.array_equal(u, w)
-    c = _sys.engine(box, st)  # one call of 25 steps == 25 calls of one step
+    c = _sys.engine(box, st, params=p)  # one call of 25 steps == 25 calls of one step
     c.setup()
     c.step(25)
     sc = c.download()
