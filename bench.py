@@ -325,8 +325,15 @@ def run_b200(args, ws, rank, local):
     peak, peak_kind = peaks()
     traffic = None
     prof = os.path.join(ROOT, "profiles", "force_dram_bytes.json")
+    ncu_issue = None
     if os.path.exists(prof):
-        traffic = json.load(open(prof)).get("bytes_per_launch")
+        pj = json.load(open(prof))
+        traffic = pj.get("bytes_per_launch")
+        if "issue_slots_busy_pct" in pj:  # compute-side roofline of the same kernel (ncu)
+            ncu_issue = {"issue_slots_busy_pct": pj["issue_slots_busy_pct"],
+                         "warp_instructions_per_launch": pj.get("warp_instructions"),
+                         "dram_throughput_pct": pj.get("dram_throughput_pct"),
+                         "source": f"profiles/{pj.get('tag')}_ncu.md"}
     # full-step byte model (reported only): B = 48 + 4n + (16 + 4n)/R
     step_bytes = N_C3 * (48.0 + 4.0 * nbar + (16.0 + 4.0 * nbar) / run.rebuild_every)
     step_ms = ms / args.steps
@@ -371,7 +378,7 @@ def run_b200(args, ws, rank, local):
                      "traffic": traffic,
                      "kernel": "k_force_walk (fused Verlet epilogue)" if fused else "k_force_walk",
                      "bytes_per_launch": bytes_per_launch, "mean_row": round(nbar, 3),
-                     "launch_ms": round(force_launch_ms, 5)},
+                     "launch_ms": round(force_launch_ms, 5), "ncu_issue": ncu_issue},
         "step_roofline": {"bytes_per_step": step_bytes,
                           "achieved_gbs": round(step_bytes / (step_ms * 1e-3) / 1e9, 1),
                           "frac": round(step_bytes / (step_ms * 1e-3) / 1e9 / peak, 4)},

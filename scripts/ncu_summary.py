@@ -82,7 +82,7 @@ def main(tag):
     os.makedirs(PROF, exist_ok=True)
     agg = launches(tag)
     md = [f"# ncu summary `{tag}` (B200, --set full --clock-control none)", ""]
-    force_bytes = None
+    force_bytes, force_extra = None, {}
     for f in sorted(os.listdir(OUT)):
         if not (f.startswith("full_") and f.endswith(f"_{tag}.ncu-rep")):
             continue
@@ -110,12 +110,19 @@ def main(tag):
                 md.append(f"| DRAM bytes per launch | {rb + wb:.4g} |")
                 if "k_force" in name and force_bytes is None:
                     force_bytes = rb + wb
+                    force_extra = {
+                        "kernel_name": name,
+                        "issue_slots_busy_pct": float(d.get("sm__inst_issued.avg.pct_of_peak_sustained_active", "nan")),
+                        "warp_instructions": float(d.get("smsp__inst_executed.sum", "nan").replace(",", "")),
+                        "dram_throughput_pct": float(d.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "nan")),
+                        "l2_hit_pct": float(d.get("lts__t_sector_hit_rate.pct", "nan")),
+                    }
             except (KeyError, ValueError):
                 pass
             md.append("")
     open(os.path.join(PROF, f"{tag}_ncu.md"), "w").write("\n".join(md) + "\n")
     if force_bytes is not None:
-        json.dump({"tag": tag, "kernel": "k_force", "bytes_per_launch": force_bytes,
+        json.dump({"tag": tag, "kernel": "k_force", "bytes_per_launch": force_bytes, **force_extra,
                    "source": f"profiles/{tag}_ncu.md (dram__bytes_read.sum + dram__bytes_write.sum)"},
                   open(os.path.join(PROF, "force_dram_bytes.json"), "w"), indent=1)
     print(open(os.path.join(PROF, f"{tag}_launches.txt")).read())
