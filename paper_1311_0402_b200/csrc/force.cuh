@@ -107,7 +107,8 @@ __device__ __forceinline__ float weight_pow_f(float w, float s, int mode) {
 }
 
 constexpr int FORCE_WARPS = DPDB_FORCE_WARPS;  // warps per CTA (kernels.cuh)
-constexpr int FORCE_TILES = 2 * FORCE_WARPS;    // 32-row tiles per CTA block
+constexpr int FORCE_TPW = DPDB_FORCE_TPW;       // 32-row tiles per warp (kernels.cuh)
+constexpr int FORCE_TILES = FORCE_TPW * FORCE_WARPS;  // 32-row tiles per CTA block
 constexpr int FORCE_BLOCK = 32 * FORCE_TILES;   // B particles per block (== RB_BLOCK)
 constexpr int FQ = 64;  // per-warp pair queue (slots)
 // Forces are accumulated as 2^-18 fixed-point int32 (|F| < 8192 per particle,
@@ -349,7 +350,7 @@ constexpr int FW_Q = 160;  // < 32 leftovers + 4 x 32 hits per group
 
 template <bool GENERAL, bool BODY, int MAXN, int FUSE>
 __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceArgs a) {
-    static_assert(FORCE_TILES == 2 * FORCE_WARPS, "tile pairing assumes 2 tiles per warp");
+    static_assert(FORCE_TPW % 2 == 0, "tiles are dealt in snake order, two per round");
     __shared__ uint32_t q_j[FORCE_WARPS][FW_Q];  // j | owner lane << 27
     __shared__ float4 own_p[FORCE_WARPS][32];
     __shared__ float4 own_v[FORCE_WARPS][32];
@@ -368,8 +369,9 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceA
     uint32_t bad_tag = 0;
 
 #pragma unroll 1
-    for (int pass = 0; pass < 2; ++pass) {
-        const uint32_t tile = pass ? (uint32_t)(FORCE_TILES - 1 - warp) : (uint32_t)warp;
+    for (int pass = 0; pass < FORCE_TPW; ++pass) {
+        // snake order: warp w takes tiles w, 2W-1-w, 2W+w, 4W-1-w, ...
+        const uint32_t tile = (uint32_t)(pass * FORCE_WARPS + ((pass & 1) ? FORCE_WARPS - 1 - warp : warp));
         const uint32_t il0 = 32u * tile;
         if (il0 >= bn) continue;
         const uint32_t il = il0 + lane;

@@ -17,9 +17,13 @@
 #include <cuda_runtime.h>
 
 // warps per pair-force CTA; the force block (and the range builder's CTA
-// block) is 64 particles per warp (A/B: 8 -> 512-particle blocks, 16 -> 1024)
+// block) is 32 * TPW particles per warp (A/B: 8 warps x 2 tiles -> 512, 16 x 2 -> 1024)
 #ifndef DPDB_FORCE_WARPS
 #define DPDB_FORCE_WARPS 8
+#endif
+// 32-row tiles each warp of a force CTA takes (block = 32 * TPW * WARPS particles)
+#ifndef DPDB_FORCE_TPW
+#define DPDB_FORCE_TPW 2
 #endif
 
 #include <cstdint>
@@ -899,7 +903,7 @@ __device__ __forceinline__ float fsel(bool p, float a, float b) {
     return r;
 }
 
-constexpr int RB_BLOCK = 64 * DPDB_FORCE_WARPS;  // == FORCE_BLOCK (force.cuh)
+constexpr int RB_BLOCK = 32 * DPDB_FORCE_TPW * DPDB_FORCE_WARPS;  // == FORCE_BLOCK (force.cuh)
 constexpr int RB_THREADS = 256;
 constexpr int RB_SLOTS = 29;     // 27 stencil cells + one split by the cut-out + a trash slot
 constexpr size_t RB_SMEM = (size_t)RB_SLOTS * RB_THREADS * 6 + RB_BLOCK * 4;
