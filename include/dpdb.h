@@ -278,6 +278,10 @@ int dpdb_md_download_ghosts(dpdb_ctx* ctx, double* x, double* y, double* z, doub
  * or several GPUs; cudaMemcpyPeerAsync over NVLink between GPUs). */
 int dpdb_group_setup(dpdb_ctx* const* ctxs, int n_bricks);
 int dpdb_group_step(dpdb_ctx* const* ctxs, int n_bricks, int64_t nsteps);
+/* dpdb_group_step with every step's thermo line (combined over the bricks in
+ * brick order; the per-brick sums are reduced on the devices by the pass that
+ * applies each step's phase 2 and land in mapped pinned memory) */
+int dpdb_group_step_thermo(dpdb_ctx* const* ctxs, int n_bricks, int64_t nsteps, dpdb_thermo* out);
 
 /* NCCL transport: one brick per process (rank = coords[0] + dims[0] *
  * (coords[1] + dims[1] * coords[2])).  Rank 0 makes the id, the caller
@@ -290,6 +294,10 @@ int dpdb_nccl_unique_id(uint8_t id[DPDB_NCCL_ID_BYTES]);
 int dpdb_nccl_attach(dpdb_ctx* ctx, const uint8_t id[DPDB_NCCL_ID_BYTES], int nranks, int rank);
 int dpdb_dist_setup(dpdb_ctx* ctx);
 int dpdb_dist_step(dpdb_ctx* ctx, int64_t nsteps);
+/* dpdb_dist_step recording this brick's per-step sums: sums[5 s + 0..4] =
+ * {step, sum v_x, sum v_y, sum v_z, sum |v|^2} over its locals (the caller adds
+ * the ranks' records in rank order: kT = (S2 - |P|^2 / N) / (3 N)) */
+int dpdb_dist_step_thermo(dpdb_ctx* ctx, int64_t nsteps, double* sums);
 /* as dpdb_step_timed: device time (ms, CUDA events on the brick's stream),
  * stage_ms[0..5] = integrate, (unused), rebuild (migration + full halo + sort
  * + build), force, other (halo update), total; stage_launches likewise */

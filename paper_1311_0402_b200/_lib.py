@@ -125,10 +125,12 @@ SYMBOLS = {
     "dpdb_md_download_ghosts": (C.c_int, [C.c_void_p] + [C.c_void_p] * 7),
     "dpdb_group_setup": (C.c_int, [C.c_void_p, C.c_int]),
     "dpdb_group_step": (C.c_int, [C.c_void_p, C.c_int, C.c_int64]),
+    "dpdb_group_step_thermo": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.POINTER(Thermo)]),
     "dpdb_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "dpdb_nccl_attach": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
     "dpdb_dist_setup": (C.c_int, [C.c_void_p]),
     "dpdb_dist_step": (C.c_int, [C.c_void_p, C.c_int64]),
+    "dpdb_dist_step_thermo": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p]),
     "dpdb_dist_step_timed": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_double), C.c_void_p,
                                        C.c_void_p]),
     "dpdb_dist_thermo": (C.c_int, [C.c_void_p, C.POINTER(Thermo)]),

@@ -109,6 +109,9 @@ struct dpdb_ctx {
     uint32_t md_n_out = 0, md_n_all = 0;
     bool md_in_rebuild = false, md_pending_p2 = false;
     bool md_integrated = false;  // the next step's Verlet pass already ran in the force epilogue
+    // brick per-step thermo: record base (device-visible) and the step of record 0
+    double* md_rec = nullptr;
+    int64_t md_rec_step0 = 0, md_rec_n = 0;
     std::array<int32_t, 26> md_gcnt{};  // ghosts this brick sends per direction
     std::array<int32_t, 26> md_rcnt{};  // ghosts it receives per direction
     void *md_sbuf{}, *md_rbuf{};         // packed records out / in (device)

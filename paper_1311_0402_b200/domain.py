@@ -228,6 +228,16 @@ class BrickGroup:
     def step(self, nsteps: int = 1):
         self._check(lib().dpdb_group_step(self._arr, len(self.bricks), int(nsteps)))
 
+    def step_thermo(self, nsteps: int):
+        """dpdb_group_step_thermo: every step's thermo line (bricks combined in
+        brick order), no host sync per step."""
+        k = int(nsteps)
+        recs = (Thermo * max(k, 1))()
+        self._check(lib().dpdb_group_step_thermo(self._arr, len(self.bricks), k, recs))
+        return dict(step=np.array([recs[i].step for i in range(k)], np.int64),
+                    kbt=np.array([recs[i].kbt for i in range(k)]),
+                    momentum=np.array([tuple(recs[i].momentum) for i in range(k)]).reshape(k, 3))
+
     @property
     def n(self):
         return sum(b.n for b in self.bricks)
@@ -477,6 +487,30 @@ class NcclBrick:
         t = Thermo()
         check(lib().dpdb_dist_thermo(self.h, C.byref(t)), self.h)
         return dict(step=t.step, n=t.n, kbt=t.kbt, momentum=tuple(t.momentum))
+
+    def step_thermo(self, nsteps: int):
+        """dpdb_dist_step_thermo: K steps, each rank records its per-step sums on
+        the device (mapped pinned memory); one all-gather at the end adds the
+        ranks' records in rank order."""
+        import torch
+        k = int(nsteps)
+        mine = np.zeros((max(k, 1), 5))
+        check(lib().dpdb_dist_step_thermo(self.h, k, ptr(mine)), self.h)
+        n_loc = float(self.brick.n)
+        dev = (torch.device("cuda", self.brick.device)
+               if self.dist.get_backend(self.group) == "nccl" else torch.device("cpu"))
+        t = torch.as_tensor(np.concatenate([mine[:k].ravel(), [n_loc]]), device=dev)
+        out = [torch.zeros_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        allr = np.stack([o.cpu().numpy() for o in out])
+        n = allr[:, -1].sum()
+        sums = allr[:, :-1].reshape(self.world, k, 5)
+        tot = np.zeros((k, 4))
+        for r in range(self.world):  # rank order: deterministic
+            tot += sums[r, :, 1:]
+        p2 = (tot[:, :3] ** 2).sum(1)
+        return dict(step=sums[0, :, 0].astype(np.int64), kbt=(tot[:, 3] - p2 / n) / (3.0 * n),
+                    momentum=tot[:, :3])
 
     @property
     def current_step(self):

@@ -191,6 +191,32 @@ def test_overlapped_halo_update_is_bitwise_blocking(monkeypatch, L, dims):
         assert np.array_equal(u, w)
 
 
+@pytest.mark.parametrize("dims", [(2, 1, 1), (2, 2, 2)])
+def test_group_step_thermo_records(dims):
+    """dpdb_group_step_thermo: per-step thermo of a brick run reduced on the
+    devices (bricks combined in brick order) == the per-step group thermo;
+    the trajectory equals plain group steps bit for bit."""
+    box, obox, st = _sys.fluid((14, 13, 12), 3.0, seed=47)
+    run = dpd.RunConfig(rebuild_every=4)
+    a = group(box, st, run, dims)
+    ref = []
+    for _ in range(9):
+        a.step(1)
+        ref.append(a.thermo())
+    b = group(box, st, run, dims)
+    rec = b.step_thermo(9)
+    assert list(rec["step"]) == list(range(1, 10))
+    n = len(st[0])
+    for k, t in enumerate(ref):
+        assert abs(rec["kbt"][k] - t["kbt"]) <= 1e-12 * t["kbt"]
+        assert np.allclose(rec["momentum"][k], t["momentum"], rtol=0, atol=1e-9 * n)
+    sa, sb = a.download(), b.download()
+    for u, w in zip(sa.coord + sa.veloc + sa.force, sb.coord + sb.veloc + sb.force):
+        assert np.array_equal(u, w)
+    a.close()
+    b.close()
+
+
 def test_ghosts_are_shifted_copies_of_their_owners():
     """After setup, after ghost updates and after a rebuild every ghost
     holds its owner's x (+ a periodic image shift) and v exactly."""
@@ -299,14 +325,16 @@ def _nccl_worker(rank, world, port, dims, steps, out):
         b.upload_global(dpd.ParticleStore.from_arrays(*st))
         b.setup()
         b.step(steps)
-        ms, stage_ms, launches = b.step_timed(3, stages=True)
+        rec = b.step_thermo(2)
+        ms, stage_ms, launches = b.step_timed(1, stages=True)
         launches = int(launches[5])
         assert abs(stage_ms[5] - ms) < 1e-6 and stage_ms[3] > 0
         s = b.download_global()
         t = b.thermo()
         if rank == 0:
             np.savez(out, tag=s.tag, x=np.stack(s.coord, 1), v=np.stack(s.veloc, 1),
-                     f=np.stack(s.force, 1), kbt=t["kbt"], n=t["n"], ms=ms, launches=launches)
+                     f=np.stack(s.force, 1), kbt=t["kbt"], n=t["n"], ms=ms, launches=launches,
+                     rec_step=rec["step"], rec_kbt=rec["kbt"], rec_mom=rec["momentum"])
         b.close()
     finally:
         dist.destroy_process_group()
@@ -335,3 +363,9 @@ def test_nccl_brick_single_rank_matches_group(tmp_path):
     t = g.thermo()
     assert abs(float(r["kbt"]) - t["kbt"]) < 1e-12 and int(r["n"]) == len(st[0])
     assert float(r["ms"]) > 0 and int(r["launches"]) > 0
+    # dpdb_dist_step_thermo records of steps 10, 11 == the group's records
+    g2 = group(box, st, dpd.RunConfig(rebuild_every=4), (1, 1, 1), steps=9)
+    rg = g2.step_thermo(2)
+    assert list(r["rec_step"]) == [10, 11] == list(rg["step"])
+    assert np.allclose(r["rec_kbt"], rg["kbt"], rtol=1e-14, atol=0)
+    assert np.allclose(r["rec_mom"], rg["momentum"], rtol=0, atol=1e-9)
