@@ -1117,7 +1117,7 @@ __global__ void __launch_bounds__(RB_THREADS, 4) k_build_range(BuildArgs a) {
             adv(j1, v1);
             p1 = __ldg(a.pos4 + j1);
         }
-        cnt[pass] = nc | (nsk << 16);
+        cnt[pass] = min(nc, 0xFFFFu) | (min(nsk, 0xFFFFu) << 16);  // saturate: >= 65535 overflows maxn anyway
         kfs[pass] = kf;
     }
     __syncthreads();
