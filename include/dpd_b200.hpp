@@ -143,9 +143,15 @@ struct PairParams {
 struct Bond {
     std::uint32_t tag_i, tag_j;
     double k, r0;
+    std::uint8_t style = 0;  // 0 harmonic, 1 FENE with R0 = r0 (unpinned)
+};
+struct Angle {  // harmonic angle around the middle tag_b (unpinned)
+    std::uint32_t tag_a, tag_b, tag_c;
+    double k, theta0;
 };
 struct BondTopology {
     std::vector<Bond> bonds;
+    std::vector<Angle> angles;
 };
 
 struct RunConfig {
@@ -252,6 +258,28 @@ public:
     void setup_at(std::int64_t step, bool keep_forces) { ck(dpdb_setup_at(ctx_, step, keep_forces)); }
     void upload_forces(const ParticleStore& s) {
         ck(dpdb_upload_forces(ctx_, s.force[0].data(), s.force[1].data(), s.force[2].data()));
+    }
+    // bonded topology (inc/core.hpp:70-81; FENE and angles beyond the reference)
+    void set_topology(const BondTopology& t) {
+        std::vector<std::uint32_t> bi, bj, aa, ab, ac;
+        std::vector<double> bk, br, ak, at;
+        std::vector<std::uint8_t> bs;
+        for (const auto& b : t.bonds) {
+            bi.push_back(b.tag_i);
+            bj.push_back(b.tag_j);
+            bk.push_back(b.k);
+            br.push_back(b.r0);
+            bs.push_back(b.style);
+        }
+        for (const auto& q : t.angles) {
+            aa.push_back(q.tag_a);
+            ab.push_back(q.tag_b);
+            ac.push_back(q.tag_c);
+            ak.push_back(q.k);
+            at.push_back(q.theta0);
+        }
+        ck(dpdb_set_bonds_styled(ctx_, bi.size(), bi.data(), bj.data(), bk.data(), br.data(), bs.data()));
+        ck(dpdb_set_angles(ctx_, aa.size(), aa.data(), ab.data(), ac.data(), ak.data(), at.data()));
     }
     // velocity_profile accumulation
     void profile_reset(std::uint32_t bins, int bin_axis, int vel_axis) {

@@ -133,6 +133,16 @@ int dpdb_init_random(dpdb_ctx* ctx, size_t n, double kbt, uint32_t seed, uint32_
                      double r0, double bond_k);
 int dpdb_set_bonds(dpdb_ctx* ctx, size_t nb, const uint32_t* tag_i, const uint32_t* tag_j,
                    const double* k, const double* r0);
+/* bonds with a style per bond: 0 harmonic, 1 FENE
+ * F = -K r / (1 - (r/R0)^2), R0 given in r0 (no reference implementation:
+ * the standard formula, unpinned; r >= R0 is a physics error) */
+int dpdb_set_bonds_styled(dpdb_ctx* ctx, size_t nb, const uint32_t* ti, const uint32_t* tj,
+                          const double* k, const double* r0, const uint8_t* style);
+/* harmonic angles U = K (theta - theta0)^2 / 2 around the middle tag tb of
+ * (ta, tb, tc), theta0 in radians (unpinned: no reference implementation);
+ * evaluated per particle with the bonds (no atomics) */
+int dpdb_set_angles(dpdb_ctx* ctx, size_t na, const uint32_t* ta, const uint32_t* tb,
+                    const uint32_t* tc, const double* k, const double* theta0);
 
 /* ------------------------------------------- per-stage entry points */
 /* sort keys of the current (unsorted) state, src/cell_grid.cpp:168-175 */

@@ -72,6 +72,8 @@ SYMBOLS = {
     "dpdb_download": (C.c_int, [C.c_void_p] + [C.c_void_p] * 12),
     "dpdb_size": (C.c_int, [C.c_void_p, C.POINTER(C.c_size_t)]),
     "dpdb_set_bonds": (C.c_int, [C.c_void_p, C.c_size_t] + [C.c_void_p] * 4),
+    "dpdb_set_bonds_styled": (C.c_int, [C.c_void_p, C.c_size_t] + [C.c_void_p] * 5),
+    "dpdb_set_angles": (C.c_int, [C.c_void_p, C.c_size_t] + [C.c_void_p] * 5),
     "dpdb_sort_keys": (C.c_int, [C.c_void_p, C.c_void_p]),
     "dpdb_reorder": (C.c_int, [C.c_void_p, C.c_void_p]),
     "dpdb_cell_start": (C.c_int, [C.c_void_p, C.c_void_p]),

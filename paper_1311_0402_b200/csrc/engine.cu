@@ -79,8 +79,17 @@ struct dpdb_ctx {
     // bonds (CSR by tag; index_of_tag refreshed at every permute)
     uint32_t *bond_off{}, *bond_partner{}, *index_of_tag{};
     float *bond_k{}, *bond_r0{};
-    size_t n_bonds = 0;
+    uint8_t* bond_style{};
+    // angles (CSR by tag: each angle at its three members with their role)
+    uint32_t* ang_off{};
+    uint4* ang_rec{};
+    float *ang_k{}, *ang_t0{};
+    size_t n_bonds = 0;  // bonded terms present: bonds + angles
     uint32_t max_tag = 0;
+    // host copies of the topology (both CSRs are rebuilt when either changes)
+    std::vector<uint32_t> h_bi, h_bj, h_aa, h_ab, h_ac;
+    std::vector<double> h_bk, h_br, h_ak, h_at;
+    std::vector<uint8_t> h_bs;
     // flags
     bool has_mol = false, have_sorted = false, have_table = false, tiled = true, joined = false;
     bool multi = false;  // n_species > 1: species packed into pos4.w bits 28-31
@@ -188,6 +197,10 @@ int check_device(dpdb_ctx* ctx) {
             break;
         case dpdb::EW_BOND:
             msg = "bond " + std::to_string(e.tag) + "-" + std::to_string(e.tag2) + ": missing endpoint";
+            break;
+        case dpdb::EW_FENE:
+            msg = "FENE bond " + std::to_string(e.tag) + "-" + std::to_string(e.tag2) +
+                  ": stretched to or beyond its maximum extension R0";
             break;
         default:
             msg = "device error";
@@ -531,6 +544,11 @@ dpdb::BondArgs bond_args(dpdb_ctx* ctx) {
     b.bpartner = ctx->bond_partner;
     b.bk = ctx->bond_k;
     b.br0 = ctx->bond_r0;
+    b.bstyle = ctx->bond_style;
+    b.aoff = ctx->ang_off;
+    b.arec = ctx->ang_rec;
+    b.ak = ctx->ang_k;
+    b.at0 = ctx->ang_t0;
     b.index_of_tag = ctx->index_of_tag;
     b.pos4 = ctx->pos4;
     for (int k = 0; k < 3; ++k) {
@@ -874,7 +892,8 @@ int dpdb_destroy(dpdb_ctx* ctx) {
                     ctx->cell_flags, ctx->stencil_code, ctx->cell_lo, ctx->entries, ctx->counts, ctx->fwalk, ctx->rowmeta,
                     ctx->err, ctx->red, ctx->red_out, ctx->thermo_part, ctx->blk_ghost, ctx->prof_acc,
                     ctx->tmp_u32, ctx->bond_off, ctx->bond_partner, ctx->index_of_tag,
-                    ctx->bond_k, ctx->bond_r0, ctx->md_masks, ctx->md_mig, ctx->md_slot,
+                    ctx->bond_k, ctx->bond_r0, ctx->bond_style, ctx->ang_off, ctx->ang_rec, ctx->ang_k,
+                    ctx->ang_t0, ctx->md_masks, ctx->md_mig, ctx->md_slot,
                     ctx->md_doff, ctx->md_dbase, ctx->md_mlist, ctx->md_glist};
     for (size_t q = 0; q < sizeof(ptrs) / sizeof(ptrs[0]); ++q)  // each buffer once
         if (ptrs[q] && std::find(ptrs, ptrs + q, ptrs[q]) == ptrs + q) cudaFree(ptrs[q]);
@@ -1078,19 +1097,115 @@ int dpdb_size(const dpdb_ctx* ctx, size_t* n) {
     return 0;
 }
 
+namespace {
+// rebuild both bonded CSRs (bonds at both endpoints, angles at their three
+// members) over tags 0..max_tag of either list, upload, refresh index_of_tag
+int upload_bonded(dpdb_ctx* ctx) {
+    void* old[] = {ctx->bond_off, ctx->bond_partner, ctx->index_of_tag, ctx->bond_k, ctx->bond_r0,
+                   ctx->bond_style, ctx->ang_off, ctx->ang_rec, ctx->ang_k, ctx->ang_t0};
+    for (void* p : old)
+        if (p) cudaFree(p);
+    ctx->bond_off = ctx->bond_partner = ctx->index_of_tag = ctx->ang_off = nullptr;
+    ctx->bond_k = ctx->bond_r0 = ctx->ang_k = ctx->ang_t0 = nullptr;
+    ctx->bond_style = nullptr;
+    ctx->ang_rec = nullptr;
+    const size_t nb = ctx->h_bi.size(), na = ctx->h_aa.size();
+    ctx->n_bonds = nb + na;
+    if (!ctx->n_bonds) return 0;
+    uint32_t max_tag = 0;
+    for (size_t q = 0; q < nb; ++q) max_tag = std::max({max_tag, ctx->h_bi[q], ctx->h_bj[q]});
+    for (size_t q = 0; q < na; ++q) max_tag = std::max({max_tag, ctx->h_aa[q], ctx->h_ab[q], ctx->h_ac[q]});
+    ctx->max_tag = max_tag;
+    // bonds: CSR by tag, each bond listed at both endpoints (full-list convention)
+    std::vector<uint32_t> off((size_t)max_tag + 2, 0), partner(2 * nb);
+    std::vector<float> kk(2 * nb), rr(2 * nb);
+    std::vector<uint8_t> st(2 * nb);
+    for (size_t q = 0; q < nb; ++q) {
+        off[ctx->h_bi[q] + 1]++;
+        off[ctx->h_bj[q] + 1]++;
+    }
+    for (size_t t = 1; t < off.size(); ++t) off[t] += off[t - 1];
+    std::vector<uint32_t> fill(off.begin(), off.end() - 1);
+    for (size_t q = 0; q < nb; ++q) {
+        const uint32_t ends[2][2] = {{ctx->h_bi[q], ctx->h_bj[q]}, {ctx->h_bj[q], ctx->h_bi[q]}};
+        for (auto& e : ends) {
+            const uint32_t p = fill[e[0]]++;
+            partner[p] = e[1];
+            kk[p] = (float)ctx->h_bk[q];
+            rr[p] = (float)ctx->h_br[q];
+            st[p] = ctx->h_bs[q];
+        }
+    }
+    // angles: CSR by tag, (other, other, role) at each member
+    std::vector<uint32_t> aoff((size_t)max_tag + 2, 0);
+    std::vector<uint4> arec(3 * na);
+    std::vector<float> ak(3 * na), at(3 * na);
+    for (size_t q = 0; q < na; ++q) {
+        aoff[ctx->h_aa[q] + 1]++;
+        aoff[ctx->h_ab[q] + 1]++;
+        aoff[ctx->h_ac[q] + 1]++;
+    }
+    for (size_t t = 1; t < aoff.size(); ++t) aoff[t] += aoff[t - 1];
+    std::vector<uint32_t> afill(aoff.begin(), aoff.end() - 1);
+    for (size_t q = 0; q < na; ++q) {
+        const uint32_t A = ctx->h_aa[q], B = ctx->h_ab[q], C = ctx->h_ac[q];
+        const uint4 recs[3] = {make_uint4(B, C, 0u, 0u), make_uint4(A, C, 1u, 0u), make_uint4(B, A, 2u, 0u)};
+        const uint32_t who[3] = {A, B, C};
+        for (int r = 0; r < 3; ++r) {
+            const uint32_t p = afill[who[r]]++;
+            arec[p] = recs[r];
+            ak[p] = (float)ctx->h_ak[q];
+            at[p] = (float)ctx->h_at[q];
+        }
+    }
+    int rc;
+    if ((rc = dalloc(ctx, ctx->bond_off, off.size())) || (rc = dalloc(ctx, ctx->bond_partner, std::max<size_t>(2 * nb, 1))) ||
+        (rc = dalloc(ctx, ctx->bond_k, std::max<size_t>(2 * nb, 1))) ||
+        (rc = dalloc(ctx, ctx->bond_r0, std::max<size_t>(2 * nb, 1))) ||
+        (rc = dalloc(ctx, ctx->bond_style, std::max<size_t>(2 * nb, 1))) ||
+        (rc = dalloc(ctx, ctx->index_of_tag, (size_t)max_tag + 1)))
+        return rc;
+    CK(cudaMemcpy(ctx->bond_off, off.data(), off.size() * 4, cudaMemcpyHostToDevice));
+    if (nb) {
+        CK(cudaMemcpy(ctx->bond_partner, partner.data(), partner.size() * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->bond_k, kk.data(), kk.size() * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->bond_r0, rr.data(), rr.size() * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->bond_style, st.data(), st.size(), cudaMemcpyHostToDevice));
+    }
+    if (na) {
+        if ((rc = dalloc(ctx, ctx->ang_off, aoff.size())) || (rc = dalloc(ctx, ctx->ang_rec, 3 * na)) ||
+            (rc = dalloc(ctx, ctx->ang_k, 3 * na)) || (rc = dalloc(ctx, ctx->ang_t0, 3 * na)))
+            return rc;
+        CK(cudaMemcpy(ctx->ang_off, aoff.data(), aoff.size() * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->ang_rec, arec.data(), arec.size() * sizeof(uint4), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->ang_k, ak.data(), ak.size() * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->ang_t0, at.data(), at.size() * 4, cudaMemcpyHostToDevice));
+    }
+    TRY(refresh_bond_index(ctx));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return 0;
+}
+}  // namespace
+
 int dpdb_set_bonds(dpdb_ctx* ctx, size_t nb, const uint32_t* ti, const uint32_t* tj, const double* k,
                    const double* r0) {
+    return dpdb_set_bonds_styled(ctx, nb, ti, tj, k, r0, nullptr);
+}
+
+int dpdb_set_bonds_styled(dpdb_ctx* ctx, size_t nb, const uint32_t* ti, const uint32_t* tj,
+                          const double* k, const double* r0, const uint8_t* style) {
     TRY(require_ctx(ctx));
     CK(cudaSetDevice(ctx->device));
     // BondTopology::validate, src/core.cpp:104-114
-    uint32_t max_tag = 0;
     std::vector<std::pair<uint32_t, uint32_t>> seen;
     seen.reserve(nb);
     for (size_t b = 0; b < nb; ++b) {
         if (ti[b] == tj[b])
             return fail(ctx, DPDB_ECONFIG, "bond topology: self bond on tag " + std::to_string(ti[b]));
+        if (style && style[b] > 1) return fail(ctx, DPDB_ECONFIG, "bond topology: style must be 0 (harmonic) or 1 (FENE)");
+        if (style && style[b] == 1 && !(r0[b] > 0))
+            return fail(ctx, DPDB_ECONFIG, "bond topology: FENE needs a positive maximum extension R0");
         seen.emplace_back(std::min(ti[b], tj[b]), std::max(ti[b], tj[b]));
-        max_tag = std::max(max_tag, std::max(ti[b], tj[b]));
     }
     std::sort(seen.begin(), seen.end());
     for (size_t b = 1; b < seen.size(); ++b)
@@ -1098,45 +1213,29 @@ int dpdb_set_bonds(dpdb_ctx* ctx, size_t nb, const uint32_t* ti, const uint32_t*
             return fail(ctx, DPDB_ECONFIG, "bond topology: duplicate bond " +
                                                std::to_string(seen[b].first) + "-" +
                                                std::to_string(seen[b].second));
-    void* old[] = {ctx->bond_off, ctx->bond_partner, ctx->index_of_tag, ctx->bond_k, ctx->bond_r0};
-    for (void* p : old)
-        if (p) cudaFree(p);
-    ctx->bond_off = ctx->bond_partner = ctx->index_of_tag = nullptr;
-    ctx->bond_k = ctx->bond_r0 = nullptr;
-    ctx->n_bonds = nb;
-    if (!nb) return 0;
-    // CSR by tag: each bond listed at both endpoints (full-list convention)
-    std::vector<uint32_t> off((size_t)max_tag + 2, 0), partner(2 * nb);
-    std::vector<float> kk(2 * nb), rr(2 * nb);
-    for (size_t b = 0; b < nb; ++b) {
-        off[ti[b] + 1]++;
-        off[tj[b] + 1]++;
-    }
-    for (size_t t = 1; t < off.size(); ++t) off[t] += off[t - 1];
-    std::vector<uint32_t> fill(off.begin(), off.end() - 1);
-    for (size_t b = 0; b < nb; ++b) {
-        uint32_t p = fill[ti[b]]++;
-        partner[p] = tj[b];
-        kk[p] = (float)k[b];
-        rr[p] = (float)r0[b];
-        p = fill[tj[b]]++;
-        partner[p] = ti[b];
-        kk[p] = (float)k[b];
-        rr[p] = (float)r0[b];
-    }
-    ctx->max_tag = max_tag;
-    int rc;
-    if ((rc = dalloc(ctx, ctx->bond_off, off.size())) || (rc = dalloc(ctx, ctx->bond_partner, 2 * nb)) ||
-        (rc = dalloc(ctx, ctx->bond_k, 2 * nb)) || (rc = dalloc(ctx, ctx->bond_r0, 2 * nb)) ||
-        (rc = dalloc(ctx, ctx->index_of_tag, (size_t)max_tag + 1)))
-        return rc;
-    CK(cudaMemcpy(ctx->bond_off, off.data(), off.size() * 4, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->bond_partner, partner.data(), partner.size() * 4, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->bond_k, kk.data(), kk.size() * 4, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->bond_r0, rr.data(), rr.size() * 4, cudaMemcpyHostToDevice));
-    TRY(refresh_bond_index(ctx));
-    CK(cudaStreamSynchronize(ctx->stream));
-    return 0;
+    ctx->h_bi.assign(ti, ti + nb);
+    ctx->h_bj.assign(tj, tj + nb);
+    ctx->h_bk.assign(k, k + nb);
+    ctx->h_br.assign(r0, r0 + nb);
+    ctx->h_bs.assign(nb, 0);
+    if (style) ctx->h_bs.assign(style, style + nb);
+    return upload_bonded(ctx);
+}
+
+int dpdb_set_angles(dpdb_ctx* ctx, size_t na, const uint32_t* ta, const uint32_t* tb,
+                    const uint32_t* tc, const double* k, const double* theta0) {
+    TRY(require_ctx(ctx));
+    CK(cudaSetDevice(ctx->device));
+    for (size_t q = 0; q < na; ++q)
+        if (ta[q] == tb[q] || tb[q] == tc[q] || ta[q] == tc[q])
+            return fail(ctx, DPDB_ECONFIG, "angle topology: three distinct tags needed at angle " +
+                                               std::to_string(q));
+    ctx->h_aa.assign(ta, ta + na);
+    ctx->h_ab.assign(tb, tb + na);
+    ctx->h_ac.assign(tc, tc + na);
+    ctx->h_ak.assign(k, k + na);
+    ctx->h_at.assign(theta0, theta0 + na);
+    return upload_bonded(ctx);
 }
 
 int dpdb_sort_keys(dpdb_ctx* ctx, uint32_t* keys) {

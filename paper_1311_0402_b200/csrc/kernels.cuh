@@ -46,6 +46,7 @@ enum ErrWhat : int {
     EW_OVERFLOW = 4,
     EW_COINCIDENT = 5,
     EW_BOND = 6,
+    EW_FENE = 7,
 };
 
 __device__ __forceinline__ void raise_err(DevErr* e, int code, int what, uint32_t t1, uint32_t t2) {
@@ -1184,6 +1185,11 @@ struct BondArgs {
     const uint32_t* bpartner;   // partner tag
     const float* bk;
     const float* br0;
+    const uint8_t* bstyle;      // 0 harmonic, 1 FENE (unpinned)
+    const uint32_t* aoff;       // angles: [max_tag + 2] CSR over tags, or null
+    const uint4* arec;          // (tag of the first other, tag of the second other, role, 0)
+    const float* ak;
+    const float* at0;
     const uint32_t* index_of_tag;
     const float4* pos4;
     float* f[3];
@@ -1194,15 +1200,34 @@ struct BondArgs {
     uint32_t tag_mask;  // 0x0FFFFFFF when species ride in pos4.w
 };
 
-// harmonic bond force on particle i (every bond of i, in CSR order); false if
-// the particle has no bonds.  Shared by k_bonds and the pair kernel epilogue.
+__device__ __forceinline__ void bonded_delta(const BondArgs& a, const float4& p, const float4& q,
+                                             float d[3]) {
+    d[0] = p.x - q.x;
+    d[1] = p.y - q.y;
+    d[2] = p.z - q.z;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        if (a.periodic[k]) d[k] = min_image_f(d[k], a.L[k], a.H[k]);
+}
+
+// Bonded force on particle i: every bond of i in CSR order -- harmonic
+// F = -K (r - r0) e or FENE F = -K r / (1 - (r / R0)^2) e (R0 in the
+// r0 slot; r >= R0 is a physics error) -- then every angle i belongs to, a
+// harmonic angle U = K (theta - theta0)^2 / 2 around the middle bead b of
+// (a, b, c): F_a = K (theta - theta0) / sin(theta) (r2 / (|r1||r2|) - cos(theta)
+// r1 / |r1|^2) with r1 = x_a - x_b, r2 = x_c - x_b, F_c likewise, F_b = -(F_a + F_c).
+// FENE and angles have no reference implementation (SURVEY hard part 7:
+// restated from the standard formulas, unpinned).  false if i has no bonded
+// term.  Shared by k_bonds and the pair kernel epilogue (no atomics: each
+// particle sums its own terms).
 __device__ __forceinline__ bool bond_force(const BondArgs& a, uint32_t i, float& fx, float& fy,
                                            float& fz) {
     const float4 pi = a.pos4[i];
     const uint32_t tag = __float_as_uint(pi.w) & a.tag_mask;
     if (tag > a.max_tag) return false;
     const uint32_t b0 = a.boff[tag], b1 = a.boff[tag + 1];
-    if (b0 == b1) return false;
+    const uint32_t e0 = a.aoff ? a.aoff[tag] : 0u, e1 = a.aoff ? a.aoff[tag + 1] : 0u;
+    if (b0 == b1 && e0 == e1) return false;
     fx = fy = fz = 0.f;
     for (uint32_t b = b0; b < b1; ++b) {
         const uint32_t pt = a.bpartner[b];
@@ -1211,16 +1236,63 @@ __device__ __forceinline__ bool bond_force(const BondArgs& a, uint32_t i, float&
             raise_err(a.err, DPDB_EPHYSICS, EW_BOND, tag, pt);
             continue;
         }
-        const float4 pj = a.pos4[j];
-        float d[3] = {pi.x - pj.x, pi.y - pj.y, pi.z - pj.z};
-#pragma unroll
-        for (int k = 0; k < 3; ++k)
-            if (a.periodic[k]) d[k] = min_image_f(d[k], a.L[k], a.H[k]);
+        float d[3];
+        bonded_delta(a, pi, a.pos4[j], d);
         const float r = sqrtf(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-        const float cc = r > 0.f ? -a.bk[b] * (r - a.br0[b]) / r : 0.f;
+        float cc;
+        if (a.bstyle && a.bstyle[b] == 1) {  // FENE
+            const float x = r / a.br0[b];
+            if (!(x < 1.f)) {
+                raise_err(a.err, DPDB_EPHYSICS, EW_FENE, tag, pt);
+                continue;
+            }
+            cc = -a.bk[b] / (1.f - x * x);
+        } else {
+            cc = r > 0.f ? -a.bk[b] * (r - a.br0[b]) / r : 0.f;
+        }
         fx += cc * d[0];
         fy += cc * d[1];
         fz += cc * d[2];
+    }
+    for (uint32_t e = e0; e < e1; ++e) {
+        const uint4 rec = a.arec[e];
+        const uint32_t j1 = a.index_of_tag[rec.x], j2 = a.index_of_tag[rec.y];
+        if (j1 >= a.n || j2 >= a.n) {
+            raise_err(a.err, DPDB_EPHYSICS, EW_BOND, tag, j1 >= a.n ? rec.x : rec.y);
+            continue;
+        }
+        // roles: 0 -> i is end a (others: b, c); 1 -> i is the middle b (a, c);
+        // 2 -> i is end c (b, a)
+        const float4 q1 = a.pos4[j1], q2 = a.pos4[j2];
+        const float4 pa = rec.z == 1 ? q1 : pi;
+        const float4 pb = rec.z == 1 ? pi : q1;
+        const float4 pc = q2;  // role 0: c; role 1: c; role 2: a (symmetric in a <-> c)
+        float r1[3], r2[3];
+        bonded_delta(a, pa, pb, r1);
+        bonded_delta(a, pc, pb, r2);
+        const float l1 = sqrtf(r1[0] * r1[0] + r1[1] * r1[1] + r1[2] * r1[2]);
+        const float l2 = sqrtf(r2[0] * r2[0] + r2[1] * r2[1] + r2[2] * r2[2]);
+        if (!(l1 > 0.f && l2 > 0.f)) continue;
+        float c = (r1[0] * r2[0] + r1[1] * r2[1] + r1[2] * r2[2]) / (l1 * l2);
+        c = fminf(fmaxf(c, -1.f), 1.f);
+        const float th = acosf(c);
+        const float sn = fmaxf(sqrtf(fmaxf(1.f - c * c, 0.f)), 1e-6f);
+        const float g = a.ak[e] * (th - a.at0[e]) / sn;
+        float fa[3], fc[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            fa[k] = g * (r2[k] / (l1 * l2) - c * r1[k] / (l1 * l1));
+            fc[k] = g * (r1[k] / (l1 * l2) - c * r2[k] / (l2 * l2));
+        }
+        if (rec.z == 1) {  // middle bead
+            fx -= fa[0] + fc[0];
+            fy -= fa[1] + fc[1];
+            fz -= fa[2] + fc[2];
+        } else {  // an end (roles 0 and 2 are mirror images: pa is this particle)
+            fx += fa[0];
+            fy += fa[1];
+            fz += fa[2];
+        }
     }
     return true;
 }

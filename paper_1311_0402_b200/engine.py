@@ -273,11 +273,28 @@ class Engine:
         self._check(lib().dpdb_download(self.h, *[ptr(x) for x in arrs], None, None, None,
                                         None, None, None))
 
-    def set_bonds(self, tag_i, tag_j, k, r0):
+    BOND_HARMONIC, BOND_FENE = 0, 1
+
+    def set_bonds(self, tag_i, tag_j, k, r0, style=None):
+        """Bond topology (inc/core.hpp:70-79).  style per bond: 0 harmonic
+        (default), 1 FENE with R0 in r0 (unpinned)."""
         ti, tj = (np.ascontiguousarray(t, np.uint32) for t in (tag_i, tag_j))
         kk, rr = (np.ascontiguousarray(np.broadcast_to(np.asarray(v, np.float64), ti.shape))
                   for v in (k, r0))
-        self._check(lib().dpdb_set_bonds(self.h, len(ti), ptr(ti), ptr(tj), ptr(kk), ptr(rr)))
+        if style is None:
+            self._check(lib().dpdb_set_bonds(self.h, len(ti), ptr(ti), ptr(tj), ptr(kk), ptr(rr)))
+        else:
+            st = np.ascontiguousarray(np.broadcast_to(np.asarray(style, np.uint8), ti.shape))
+            self._check(lib().dpdb_set_bonds_styled(self.h, len(ti), ptr(ti), ptr(tj), ptr(kk), ptr(rr),
+                                                    ptr(st)))
+
+    def set_angles(self, tag_a, tag_b, tag_c, k, theta0):
+        """Harmonic angles U = K (theta - theta0)^2 / 2 around the middle tag_b
+        (unpinned: no reference implementation)."""
+        ta, tb, tc = (np.ascontiguousarray(t, np.uint32) for t in (tag_a, tag_b, tag_c))
+        kk, t0 = (np.ascontiguousarray(np.broadcast_to(np.asarray(v, np.float64), ta.shape))
+                  for v in (k, theta0))
+        self._check(lib().dpdb_set_angles(self.h, len(ta), ptr(ta), ptr(tb), ptr(tc), ptr(kk), ptr(t0)))
 
     # -------------------------------------------------- stage entry points
     def sort_keys(self):

@@ -17,7 +17,10 @@ whitespace separated.  Species-pair overrides are `a.X.Y = v` / `gamma.X.Y = v`
   [run]     dt*, steps*, rebuild_every (10), skin (0.3), body_force (0),
             drive_axis (0), partition_axis (2), max_neighbors (128),
             wall_mode (specular | bounce_back)
-  [chains]  fraction*, sequence*, r0 (0.38), k (80), solvent (first species)
+  [chains]  fraction*, sequence*, r0 (0.38), k (80), solvent (first species),
+            bond (harmonic | fene: FENE with maximum extension fene_r0),
+            angle_k, angle_theta0 (degrees; harmonic angles along the chains)
+            -- FENE and angles go beyond the reference (unpinned)
   [profile] bins (50), axis (2), every (100), start (0)
 (* required; chains/profile sections optional)
 """
@@ -37,7 +40,8 @@ _KEYS = {
     "pair": {"a", "sigma", "gamma", "r_c", "s"},
     "run": {"dt", "steps", "rebuild_every", "skin", "body_force", "drive_axis", "partition_axis",
             "max_neighbors", "wall_mode"},
-    "chains": {"fraction", "sequence", "r0", "k", "solvent"},
+    "chains": {"fraction", "sequence", "r0", "k", "solvent", "bond", "fene_r0", "angle_k",
+               "angle_theta0"},
     "profile": {"bins", "axis", "every", "start"},
 }
 _REQUIRED = [("box", "hi"), ("fluid", "kbt"), ("pair", "a"), ("run", "dt"), ("run", "steps")]
@@ -72,6 +76,14 @@ class Scenario:
             e.init_random(self.n, self.kbt, self.seed, self.n_chains, seq,
                           self.species.index(self.chains["solvent"]), self.chains["r0"],
                           self.chains["k"])
+            c, m = self.chains, len(seq)
+            first = np.arange(self.n_chains) * m + 1  # tags of bead 0
+            if c["bond"] == "fene":
+                ti = (first[:, None] + np.arange(m - 1)[None, :]).ravel()
+                e.set_bonds(ti, ti + 1, c["k"], c["fene_r0"], style=Engine.BOND_FENE)
+            if c["angle_k"] > 0 and m >= 3:
+                ta = (first[:, None] + np.arange(m - 2)[None, :]).ravel()
+                e.set_angles(ta, ta + 1, ta + 2, c["angle_k"], np.deg2rad(c["angle_theta0"]))
         else:
             e.init_random(self.n, self.kbt, self.seed)
         return e
@@ -202,7 +214,15 @@ def parse_text(text: str, source: str = "<string>") -> Scenario:
         if not 0 < frac <= 1:
             raise DPDError(1, "config: chains.fraction must be in (0, 1]")
         chains = dict(fraction=frac, sequence=seq, r0=_num(c.get("r0", "0.38"), "chains.r0"),
-                      k=_num(c.get("k", "80"), "chains.k"), solvent=c.get("solvent", species[0]))
+                      k=_num(c.get("k", "80"), "chains.k"), solvent=c.get("solvent", species[0]),
+                      bond=c.get("bond", "harmonic"),
+                      fene_r0=_num(c.get("fene_r0", "1.5"), "chains.fene_r0"),
+                      angle_k=_num(c.get("angle_k", "0"), "chains.angle_k"),
+                      angle_theta0=_num(c.get("angle_theta0", "180"), "chains.angle_theta0"))
+        if chains["bond"] not in ("harmonic", "fene"):
+            raise DPDError(1, "config: chains.bond must be harmonic or fene")
+        if chains["bond"] == "fene" and not chains["fene_r0"] > chains["r0"]:
+            raise DPDError(1, "config: chains.fene_r0 must exceed the initial bond length r0")
         if chains["solvent"] not in species:
             raise DPDError(1, "config: chains.solvent is not a species")
     profile = None

@@ -167,3 +167,83 @@ def test_coincident_particles_error():
     with pytest.raises(dpd.DPDError) as ex:
         e.compute_forces(0)
     assert ex.value.code == 2
+
+
+def _bonded_reference(X, L, bonds, angles):
+    """fp64 forces of FENE / harmonic bonds and harmonic angles from the
+    standard formulas (tags 1..n are indices + 1): -grad U."""
+    F = np.zeros_like(X)
+
+    def mi(d):
+        return d - L * np.round(d / L)
+
+    for (i, j, K, r0, style) in bonds:
+        d = mi(X[i] - X[j])
+        r = np.linalg.norm(d)
+        c = -K / (1 - (r / r0) ** 2) if style == 1 else -K * (r - r0) / r
+        F[i] += c * d
+        F[j] -= c * d
+    for (a, b, c_, K, t0) in angles:
+        r1, r2 = mi(X[a] - X[b]), mi(X[c_] - X[b])
+        l1, l2 = np.linalg.norm(r1), np.linalg.norm(r2)
+        cs = np.dot(r1, r2) / (l1 * l2)
+        th = np.arccos(np.clip(cs, -1, 1))
+        g = K * (th - t0) / np.sin(th)
+        fa = g * (r2 / (l1 * l2) - cs * r1 / l1 ** 2)
+        fc = g * (r1 / (l1 * l2) - cs * r2 / l2 ** 2)
+        F[a] += fa
+        F[c_] += fc
+        F[b] -= fa + fc
+    return F
+
+
+@pytest.mark.parametrize("pipeline", [False, True])
+def test_fene_bonds_and_angles(pipeline):
+    """North-star bonded terms beyond the reference (unpinned, standard
+    formulas): FENE bonds and harmonic angles along 6-bead chains, no pair
+    forces (a = gamma = 0), device vs fp64 -grad U; momentum conserved; the
+    fused pipeline (epilogue) and the stage API (k_bonds) agree."""
+    L = 9.0
+    rng = np.random.default_rng(4)
+    nch, m = 40, 6
+    n = nch * m + 200
+    X = rng.uniform(0, L, (n, 3))
+    for c in range(nch):  # random walks with step 0.9 (inside R0 = 1.5)
+        for b in range(1, m):
+            u = rng.normal(size=3)
+            X[c * m + b] = (X[c * m + b - 1] + 0.9 * u / np.linalg.norm(u)) % L
+    bonds, angles = [], []
+    for c in range(nch):
+        for b in range(m - 1):
+            i = c * m + b
+            bonds.append((i, i + 1, 30.0, 1.5, 1))
+        for b in range(m - 2):
+            i = c * m + b
+            angles.append((i, i + 1, i + 2, 5.0, 2.0))
+    box = dpd.SimBox((0.0, 0.0, 0.0), (L, L, L))
+    p = dpd.PairParams.make(1, 0.0, 0.0, 0.0, 1.0, 1.0, 0.01)
+    z = np.zeros(n)
+    e = dpd.Engine(box, p, dpd.RunConfig(), capacity=n)
+    e.upload(dpd.ParticleStore.from_arrays(X[:, 0], X[:, 1], X[:, 2], z, z, z, np.arange(1, n + 1)))
+    bi = np.array([b[0] + 1 for b in bonds]); bj = np.array([b[1] + 1 for b in bonds])
+    e.set_bonds(bi, bj, 30.0, 1.5, style=1)
+    ai, ab, ac = (np.array([a[q] + 1 for a in angles]) for q in range(3))
+    e.set_angles(ai, ab, ac, 5.0, 2.0)
+    if pipeline:
+        e.setup()
+        s = e.download()
+    else:
+        e.reorder_particles()
+        e.build_neighbor_table()
+        e.compute_forces(0)
+        s = e.download()
+    o = np.argsort(s.tag)
+    Fg = np.stack(s.force, 1)[o]
+    Fr = _bonded_reference(X, L, bonds, angles)
+    assert np.linalg.norm(Fg - Fr) / np.linalg.norm(Fr) < 1e-5
+    assert np.abs(Fg.sum(0)).max() < 1e-3 * np.abs(Fg).max()
+    # FENE beyond R0 is a physics error
+    e.set_bonds([1], [2], 30.0, 0.1, style=1)
+    with pytest.raises(dpd.DPDError) as ex:
+        e.compute_forces(0)
+    assert ex.value.code == 2 and "FENE" in str(ex.value)

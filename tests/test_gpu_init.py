@@ -89,3 +89,45 @@ def test_self_assembly_aggregates():
     c1 = biggest()
     assert c1[1] > 50 and c1[1] >= 3 * c0[1], (c0, c1)
     assert abs(e.thermo()["kbt"] - 1.0) < 0.03
+
+
+def test_fene_angle_chains_run_stably(tmp_path):
+    """A scenario with FENE chains and harmonic angles (beyond the reference)
+    runs: bonds stay inside R0, temperature stays at kT."""
+    from paper_1311_0402_b200.scenario import parse_text
+    s = parse_text("""[box]
+hi = 12 12 12
+[fluid]
+density = 3
+kbt = 1
+seed = 2
+species = S A B
+[pair]
+gamma = 4.5
+a = 25
+a.A.B = 50
+[run]
+dt = 0.01
+steps = 2000
+[chains]
+fraction = 0.2
+sequence = BBBAABBB
+r0 = 0.5
+k = 20
+bond = fene
+fene_r0 = 1.5
+angle_k = 3
+angle_theta0 = 180
+""")
+    e = s.engine()
+    e.setup()
+    rec = e.step_thermo(2000)
+    assert abs(rec["kbt"][1000:].mean() - 1.0) < 0.05
+    st = e.download()
+    o = np.argsort(st.tag)
+    X = np.stack(st.coord, 1)[o]
+    nb = s.n_chains * 8
+    d = X[1:nb] - X[:nb - 1]
+    d -= 12.0 * np.round(d / 12.0)
+    r = np.linalg.norm(d, axis=1)[np.arange(1, nb) % 8 != 0]
+    assert r.max() < 1.5 and r.mean() < 1.2

@@ -112,11 +112,12 @@ def test_fused_force_integrate_equals_separate_pass(monkeypatch, case):
         assert np.array_equal(u, w)
 
 
-def test_bonded_pipeline_equals_stagewise_api():
-    """With harmonic bonds the step loop adds the bond forces in the pair
-    kernel's epilogue (and still fuses the Verlet pass); the stage-by-stage
-    ABI adds them with the separate k_bonds pass.  Same trajectory bit for
-    bit (three species, 8-bead chains)."""
+@pytest.mark.parametrize("extra", [False, True])
+def test_bonded_pipeline_equals_stagewise_api(extra):
+    """With bonds the step loop adds the bond forces in the pair kernel's
+    epilogue (and still fuses the Verlet pass); the stage-by-stage ABI adds
+    them with the separate k_bonds pass.  Same trajectory bit for bit (three
+    species, 8-bead chains; extra: FENE bonds + harmonic angles)."""
     L = (10.0, 10.0, 10.0)
     p = dpd.PairParams.make(3, [15, 15, 120, 15, 15, 120, 120, 120, 15], 4.5, 1.0, 1.0, 1.0, 0.01)
     box = dpd.SimBox((0.0, 0.0, 0.0), L)
@@ -125,6 +126,12 @@ def test_bonded_pipeline_equals_stagewise_api():
     def fresh():
         e = dpd.Engine(box, p, dpd.RunConfig(), capacity=n)
         e.init_random(n, 1.0, 9, nc, seq, 0, 0.38, 80.0)
+        if extra:
+            first = np.arange(nc) * 8 + 1
+            ti = (first[:, None] + np.arange(7)[None, :]).ravel()
+            e.set_bonds(ti, ti + 1, 40.0, 2.0, style=1)
+            ta = (first[:, None] + np.arange(6)[None, :]).ravel()
+            e.set_angles(ta, ta + 1, ta + 2, 4.0, np.pi)
         return e
 
     a = fresh()

@@ -30,7 +30,8 @@ def test_self_assembly_cfg():
     S, A, B = 0, 1, 2
     assert a[A, A] == a[A, S] == a[S, S] == a[B, B] == 15 and a[A, B] == a[B, A] == a[B, S] == 120
     assert np.allclose(s.params.gamma, 4.5) and np.allclose(s.params.sigma, 3.0)
-    assert s.chains == dict(fraction=0.1, sequence="BBBAABBB", r0=0.38, k=80.0, solvent="S")
+    assert s.chains == dict(fraction=0.1, sequence="BBBAABBB", r0=0.38, k=80.0, solvent="S",
+                            bond="harmonic", fene_r0=1.5, angle_k=0.0, angle_theta0=180.0)
     assert s.n_chains == round(0.1 * s.n) // 8
 
 
