@@ -446,10 +446,17 @@ int do_build(dpdb_ctx* ctx, bool joined_out) {
         const double rm = rs + 1e-3;  // margin over the fp32 frame's rounding
         a.cut_cull = (float)(rm * rm);
         const unsigned nb = (unsigned)((ctx->n + dpdb::RB_BLOCK - 1) / dpdb::RB_BLOCK);
-        if (joined_out)
-            dpdb::k_build_range<true><<<nb, dpdb::RB_THREADS, dpdb::RB_SMEM, ctx->stream>>>(a);
+        // ghost rows exist only in a brick (ghost cell layers); otherwise the
+        // per-candidate ghost-partner test is compiled out
+        const bool gh = ctx->grid.n_total_cells > ctx->grid.n_local_cells;
+        if (joined_out && gh)
+            dpdb::k_build_range<true, true><<<nb, dpdb::RB_THREADS, dpdb::RB_SMEM, ctx->stream>>>(a);
+        else if (joined_out)
+            dpdb::k_build_range<true, false><<<nb, dpdb::RB_THREADS, dpdb::RB_SMEM, ctx->stream>>>(a);
+        else if (gh)
+            dpdb::k_build_range<false, true><<<nb, dpdb::RB_THREADS, dpdb::RB_SMEM, ctx->stream>>>(a);
         else
-            dpdb::k_build_range<false><<<nb, dpdb::RB_THREADS, dpdb::RB_SMEM, ctx->stream>>>(a);
+            dpdb::k_build_range<false, false><<<nb, dpdb::RB_THREADS, dpdb::RB_SMEM, ctx->stream>>>(a);
         CKL();
         ctx->launches[ST_BUILD]++;
         return 0;
@@ -872,9 +879,13 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         cudaFuncSetAttribute(dpdb::k_build<BUILD_WARPS, BUILD_TILES, false>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return bail(fail(ctx, DPDB_ECONFIG, "max_neighbors too large for the builder's shared memory"));
-    if (cudaFuncSetAttribute(dpdb::k_build_range<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(dpdb::k_build_range<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)dpdb::RB_SMEM) != cudaSuccess ||
-        cudaFuncSetAttribute(dpdb::k_build_range<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(dpdb::k_build_range<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)dpdb::RB_SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(dpdb::k_build_range<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)dpdb::RB_SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(dpdb::k_build_range<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)dpdb::RB_SMEM) != cudaSuccess)
         return bail(fail(ctx, DPDB_EDEVICE, "range builder shared memory"));
     *out = ctx;

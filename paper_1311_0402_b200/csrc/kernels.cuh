@@ -27,6 +27,7 @@
 #endif
 
 #include <cstdint>
+#include <type_traits>
 
 #include "dpd_math.cuh"
 
@@ -907,6 +908,8 @@ __global__ void __launch_bounds__(256) k_build_lane(BuildArgs a) {
 //
 // !WALK: the reference split layout (core from the front, skin reversed from
 //        the back), counts = core | skin << 13 | flags << 26.
+// GH: the context has ghost rows (a brick); only then is each hit tested for a
+//     ghost partner (the block's blk_ghost flag).
 //  WALK: only the entries the force kernel evaluates (j outside the block or
 //        j > i), ascending, skin tagged with bit 31; fwalk = n_front | flags.
 //        The in-block j < i entries are not stored -- they are exactly the
@@ -928,7 +931,7 @@ constexpr int RB_SLOTS = 29;     // 27 stencil cells + one split by the cut-out 
 constexpr size_t RB_SMEM = (size_t)RB_SLOTS * RB_THREADS * 6 + RB_BLOCK * 4;
 constexpr uint32_t RB_NONE = 0xFFFFFFFFu;
 
-template <bool WALK>
+template <bool WALK, bool GH>
 __global__ void __launch_bounds__(RB_THREADS, 4) k_build_range(BuildArgs a) {
     extern __shared__ uint32_t rb_smem[];  // RB_SMEM bytes (dynamic: > 48 KB)
     uint32_t(*rs)[RB_THREADS] = reinterpret_cast<uint32_t(*)[RB_THREADS]>(rb_smem);
@@ -1071,6 +1074,8 @@ __global__ void __launch_bounds__(RB_THREADS, 4) k_build_range(BuildArgs a) {
         adv(j1, v1);
         float4 p0 = __ldg(a.pos4 + j0), p1 = __ldg(a.pos4 + j1);
         uint32_t* rowp = a.entries + (size_t)(i & ~31u) * maxn + (i & 31u);
+        uint32_t* wp = rowp;
+        const int wstep = 32 - 31 * (int)maxn;  // entry 32q+31 -> 32(q+1)
         uint32_t kf = 0, kb = 0, nc = 0, nsk = 0;
         const float cut_s = a.cut_s, cut_c = a.cut_c;
         // branch-free min image (min_image_f semantics): axes without wrap get
@@ -1083,41 +1088,52 @@ __global__ void __launch_bounds__(RB_THREADS, 4) k_build_range(BuildArgs a) {
             const float lo = __fsub_rn(d, L), hi = __fadd_rn(d, L);
             return d >= H ? lo : (d < -H ? hi : d);
         };
-        auto test = [&](uint32_t j, float4 pj, bool v) {
-            float dx = __fsub_rn(pi.x, pj.x);
-            float dy = __fsub_rn(pi.y, pj.y);
-            float dz = __fsub_rn(pi.z, pj.z);
-            if (anywrap) {
-                dx = mimg(dx, Lx, Hx);
-                dy = mimg(dy, Ly, Hy);
-                dz = mimg(dz, Lz, Hz);
+        // the walk is instantiated twice: warps with no wrapped row (the bulk)
+        // issue no minimum-image instructions at all
+        auto walk = [&](auto wrapc) {
+            constexpr bool WRAPW = decltype(wrapc)::value;
+            auto test = [&](uint32_t j, float4 pj, bool v) {
+                float dx = __fsub_rn(pi.x, pj.x);
+                float dy = __fsub_rn(pi.y, pj.y);
+                float dz = __fsub_rn(pi.z, pj.z);
+                if (WRAPW) {
+                    dx = mimg(dx, Lx, Hx);
+                    dy = mimg(dy, Ly, Hy);
+                    dz = mimg(dz, Lz, Hz);
+                }
+                const float d2 =
+                    __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
+                const bool hit = v && d2 <= cut_s;
+                const bool core = d2 <= cut_c;
+                if (GH && hit && j >= a.n_local) ghost_seen = 1u;  // same value from every writer
+                if (WALK) {
+                    // wp: running tile-transposed position of entry kf
+                    if (hit && kf < maxn) *wp = core ? j : (j | 0x80000000u);
+                    if (hit) wp += ((kf & 31u) == 31u) ? wstep : (int)maxn;
+                    kf += hit;
+                    if (hit && j < bend && j > i) atomicAdd(&back[j - b0], core ? 1u : 0x10000u);
+                } else {
+                    const uint32_t k = core ? kf : maxn - 1u - kb;
+                    if (hit && kf + kb < maxn) rowp[(k & 31u) * maxn + (k & ~31u)] = j;
+                    kf += hit && core;
+                    kb += hit && !core;
+                }
+                nc += hit && core;
+                nsk += hit && !core;
+            };
+            while (__any_sync(0xFFFFFFFFu, v0)) {
+                test(j0, p0, v0);
+                adv(j0, v0);
+                p0 = __ldg(a.pos4 + j0);
+                test(j1, p1, v1);
+                adv(j1, v1);
+                p1 = __ldg(a.pos4 + j1);
             }
-            const float d2 =
-                __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
-            const bool hit = v && d2 <= cut_s;
-            const bool core = d2 <= cut_c;
-            if (hit && j >= a.n_local) ghost_seen = 1u;  // same value from every writer
-            if (WALK) {
-                if (hit && kf < maxn) rowp[(kf & 31u) * maxn + (kf & ~31u)] = core ? j : (j | 0x80000000u);
-                kf += hit;
-                if (hit && j < bend && j > i) atomicAdd(&back[j - b0], core ? 1u : 0x10000u);
-            } else {
-                const uint32_t k = core ? kf : maxn - 1u - kb;
-                if (hit && kf + kb < maxn) rowp[(k & 31u) * maxn + (k & ~31u)] = j;
-                kf += hit && core;
-                kb += hit && !core;
-            }
-            nc += hit && core;
-            nsk += hit && !core;
         };
-        while (__any_sync(0xFFFFFFFFu, v0)) {
-            test(j0, p0, v0);
-            adv(j0, v0);
-            p0 = __ldg(a.pos4 + j0);
-            test(j1, p1, v1);
-            adv(j1, v1);
-            p1 = __ldg(a.pos4 + j1);
-        }
+        if (anywrap)
+            walk(std::true_type{});
+        else
+            walk(std::false_type{});
         cnt[pass] = min(nc, 0xFFFFu) | (min(nsk, 0xFFFFu) << 16);  // saturate: >= 65535 overflows maxn anyway
         kfs[pass] = kf;
     }
