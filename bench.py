@@ -348,10 +348,13 @@ def run_b200(args, ws, rank, local):
     barrier_sync(ws)
     t0 = time.perf_counter()
     e.upload(dpd.ParticleStore.from_arrays(*pinned))
+    t_up = time.perf_counter()
     e.setup()
+    t_setup = time.perf_counter()
     # every step's thermo line reaches the host (dpdb_step_thermo / dpdb_dist_step_thermo:
     # reduced on the device, records in mapped pinned memory, no per-step sync)
     rec = e.step_thermo(args.steps)
+    t_steps = time.perf_counter()
     assert len(rec["kbt"]) == args.steps and np.all(np.isfinite(rec["kbt"]))
     if bricks:
         s = e.download()
@@ -360,8 +363,11 @@ def run_b200(args, ws, rank, local):
             out[3 + k][:] = s.veloc[k]
     else:  # straight into the pinned result buffers
         e.download_state(out[0:3], out[3:6])
+    t_end = time.perf_counter()
     barrier_sync(ws)
     e2e_s = max_over_ranks(time.perf_counter() - t0, ws, local)
+    e2e_parts = {"upload": t_up - t0, "setup": t_setup - t_up, "steps": t_steps - t_setup,
+                 "download": t_end - t_steps}
     e2e = total_particles * args.steps / e2e_s / 1e6
     h2d = N_C3 * (6 * 8 + 4)
     d2h_state = N_C3 * ((9 * 8 + 4 + 1 + 4) if bricks else 6 * 8)
@@ -389,6 +395,7 @@ def run_b200(args, ws, rank, local):
         "gpu_launches": int(launches[5]),
         "e2e": {"value": round(e2e, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d / args.steps),
                 "d2h_bytes_per_step": int(d2h),
+                "wall_ms": {k: round(v * 1e3, 3) for k, v in e2e_parts.items()},
                 "note": "upload + setup + step_thermo(K) (every step's thermo record D2H into "
                         "pinned memory) + download, pinned host"},
         "clocks": clk.summary(),

@@ -302,6 +302,8 @@ int launch_integrate(dpdb_ctx* ctx, bool defer_wrap = false, bool thermo = false
     return 0;
 }
 
+constexpr size_t THERMO_RING = 4096;  // records preallocated per context
+
 int radix_sort_on(dpdb_ctx* ctx, cudaStream_t st, uint32_t*& k, uint32_t*& v, uint32_t*& k2,
                   uint32_t*& v2, uint32_t* hist, size_t n, int bits) {
     if (n == 0 || bits == 0) return 0;
@@ -888,6 +890,15 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         cudaFuncSetAttribute(dpdb::k_build_range<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)dpdb::RB_SMEM) != cudaSuccess)
         return bail(fail(ctx, DPDB_EDEVICE, "range builder shared memory"));
+    // per-step thermo records (dpdb_step_thermo): a mapped pinned ring sized
+    // for typical calls, so no host allocation lands in a step call (larger
+    // calls grow it once)
+    if (cudaHostAlloc(reinterpret_cast<void**>(&ctx->thermo_host), THERMO_RING * 5 * sizeof(double),
+                      cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->thermo_host_dev), ctx->thermo_host, 0) !=
+            cudaSuccess)
+        return bail(fail(ctx, DPDB_EDEVICE, "thermo record buffer"));
+    ctx->thermo_cap = THERMO_RING;
     *out = ctx;
     return 0;
 }

@@ -1075,6 +1075,7 @@ __global__ void __launch_bounds__(RB_THREADS, 4) k_build_range(BuildArgs a) {
         float4 p0 = __ldg(a.pos4 + j0), p1 = __ldg(a.pos4 + j1);
         uint32_t* rowp = a.entries + (size_t)(i & ~31u) * maxn + (i & 31u);
         uint32_t* wp = rowp;
+        const uint32_t back_sa = (uint32_t)__cvta_generic_to_shared(back) - 4u * b0;
         const int wstep = 32 - 31 * (int)maxn;  // entry 32q+31 -> 32(q+1)
         uint32_t kf = 0, kb = 0, nc = 0, nsk = 0;
         const float cut_s = a.cut_s, cut_c = a.cut_c;
@@ -1107,11 +1108,16 @@ __global__ void __launch_bounds__(RB_THREADS, 4) k_build_range(BuildArgs a) {
                 const bool core = d2 <= cut_c;
                 if (GH && hit && j >= a.n_local) ghost_seen = 1u;  // same value from every writer
                 if (WALK) {
-                    // wp: running tile-transposed position of entry kf
-                    if (hit && kf < maxn) *wp = core ? j : (j | 0x80000000u);
-                    if (hit) wp += ((kf & 31u) == 31u) ? wstep : (int)maxn;
+                    // predicated store / shared add (no branch per candidate)
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.global.u32 [%0], %1;\n\t}"
+                                 ::"l"(wp), "r"(core ? j : (j | 0x80000000u)),
+                                 "r"((uint32_t)(hit && kf < maxn)));
+                    wp += hit ? (((kf & 31u) == 31u) ? wstep : (int)maxn) : 0;
                     kf += hit;
-                    if (hit && j < bend && j > i) atomicAdd(&back[j - b0], core ? 1u : 0x10000u);
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.shared.add.u32 [%0], %1;\n\t}"
+                                 ::"r"(back_sa + 4u * j), "r"(core ? 1u : 0x10000u),
+                                 "r"((uint32_t)(hit && j < bend && j > i))
+                                 : "memory");
                 } else {
                     const uint32_t k = core ? kf : maxn - 1u - kb;
                     if (hit && kf + kb < maxn) rowp[(k & 31u) * maxn + (k & ~31u)] = j;
