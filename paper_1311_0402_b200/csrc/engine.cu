@@ -85,6 +85,7 @@ struct dpdb_ctx {
     uint4* ang_rec{};
     float *ang_k{}, *ang_t0{};
     size_t n_bonds = 0;  // bonded terms present: bonds + angles
+    bool styled = false;  // FENE bonds or angles: k_bonds after the pair kernel, no fusion
     uint32_t max_tag = 0;
     // host copies of the topology (both CSRs are rebuilt when either changes)
     std::vector<uint32_t> h_bi, h_bj, h_aa, h_ab, h_ac;
@@ -538,10 +539,10 @@ void force_dispatch_layout(dpdb_ctx* ctx, const dpdb::ForceArgs& a, bool body, i
 
 // Whether the step loop may run the next Verlet pass inside the force kernel:
 // single domain, walk layout with 128-slot rows (the walk kernel adds the
-// bond forces in its epilogue, so bonds fuse too).
+// harmonic bond forces in its epilogue, so those fuse too; FENE / angles do not).
 bool can_fuse(const dpdb_ctx* ctx) {
     return ctx->walk && ctx->maxn == 128 && !ctx->md_valid &&
-           ctx->dims[0] * ctx->dims[1] * ctx->dims[2] == 1 && !ctx->no_fuse;
+           ctx->dims[0] * ctx->dims[1] * ctx->dims[2] == 1 && !ctx->no_fuse && !ctx->styled;
 }
 
 // fuse (step loop only, can_fuse): FUSE_STREAMS / FUSE_KEYS run phase 2 of
@@ -611,7 +612,9 @@ int do_forces(dpdb_ctx* ctx, uint32_t step, int fuse = dpdb::FUSE_NONE, bool the
         a.tg[q] = (float)p.gamma[q];
         a.ts[q] = (float)(ctx->sigma[q] / std::sqrt(p.dt));
     }
-    if (ctx->n_bonds && ctx->walk) {
+    // harmonic bonds ride in the walk kernel's epilogue; FENE and angles need k_bonds
+    const bool bonds_after = ctx->n_bonds && (!ctx->walk || ctx->styled);
+    if (ctx->n_bonds && !bonds_after) {
         a.has_bonds = 1;
         a.bd = bond_args(ctx);
     }
@@ -631,7 +634,7 @@ int do_forces(dpdb_ctx* ctx, uint32_t step, int fuse = dpdb::FUSE_NONE, bool the
         force_dispatch_layout<false>(ctx, a, body, fuse);
     CKL();
     ctx->launches[ST_FORCE]++;
-    if (ctx->n_bonds && !ctx->walk) {  // the walk kernel added them in its epilogue
+    if (bonds_after && part != 0) {  // split force pass: once, after the boundary part
         dpdb::BondArgs b = bond_args(ctx);
         dpdb::k_bonds<<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(b);
         CKL();
@@ -1133,6 +1136,8 @@ int upload_bonded(dpdb_ctx* ctx) {
     ctx->ang_rec = nullptr;
     const size_t nb = ctx->h_bi.size(), na = ctx->h_aa.size();
     ctx->n_bonds = nb + na;
+    ctx->styled = na > 0;
+    for (size_t q = 0; q < nb && !ctx->styled; ++q) ctx->styled = ctx->h_bs[q] != 0;
     if (!ctx->n_bonds) return 0;
     uint32_t max_tag = 0;
     for (size_t q = 0; q < nb; ++q) max_tag = std::max({max_tag, ctx->h_bi[q], ctx->h_bj[q]});

@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceA
     for (int q = 0; q < PER_T; ++q) {
         const uint32_t t = threadIdx.x + q * FORCE_WARPS * 32;
         bset[q] = GENERAL && a.has_bonds && t < bn &&
-                  bond_force(a.bd, b0 + t, bf[q][0], bf[q][1], bf[q][2]);
+                  bond_force<false>(a.bd, b0 + t, bf[q][0], bf[q][1], bf[q][2]);
     }
     if (FUSE != FUSE_NONE) {
 #pragma unroll

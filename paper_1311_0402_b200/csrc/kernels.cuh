@@ -1242,15 +1242,21 @@ __device__ __forceinline__ void bonded_delta(const BondArgs& a, const float4& p,
 // restated from the standard formulas, unpinned).  false if i has no bonded
 // term.  Shared by k_bonds and the pair kernel epilogue (no atomics: each
 // particle sums its own terms).
+// STYLED: bond styles (FENE) and angle terms too (k_bonds).  The pair
+// kernel's fused epilogue carries harmonic bonds alone (STYLED = false), so
+// its register allocation does not pay for the rest; contexts with FENE bonds
+// or angles run k_bonds after the pair kernel, unfused.
+template <bool STYLED>
 __device__ __forceinline__ bool bond_force(const BondArgs& a, uint32_t i, float& fx, float& fy,
                                            float& fz) {
     const float4 pi = a.pos4[i];
     const uint32_t tag = __float_as_uint(pi.w) & a.tag_mask;
     if (tag > a.max_tag) return false;
     const uint32_t b0 = a.boff[tag], b1 = a.boff[tag + 1];
-    const uint32_t e0 = a.aoff ? a.aoff[tag] : 0u, e1 = a.aoff ? a.aoff[tag + 1] : 0u;
+    const uint32_t e0 = STYLED && a.aoff ? a.aoff[tag] : 0u, e1 = STYLED && a.aoff ? a.aoff[tag + 1] : 0u;
     if (b0 == b1 && e0 == e1) return false;
     fx = fy = fz = 0.f;
+    uint32_t fene_bad = 0;  // partner tag of an overstretched FENE bond (raised once)
     for (uint32_t b = b0; b < b1; ++b) {
         const uint32_t pt = a.bpartner[b];
         const uint32_t j = a.index_of_tag[pt];
@@ -1261,22 +1267,19 @@ __device__ __forceinline__ bool bond_force(const BondArgs& a, uint32_t i, float&
         float d[3];
         bonded_delta(a, pi, a.pos4[j], d);
         const float r = sqrtf(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-        float cc;
-        if (a.bstyle && a.bstyle[b] == 1) {  // FENE
-            const float x = r / a.br0[b];
-            if (!(x < 1.f)) {
-                raise_err(a.err, DPDB_EPHYSICS, EW_FENE, tag, pt);
-                continue;
-            }
-            cc = -a.bk[b] / (1.f - x * x);
-        } else {
-            cc = r > 0.f ? -a.bk[b] * (r - a.br0[b]) / r : 0.f;
-        }
+        const float k = a.bk[b], r0 = a.br0[b];
+        const bool fene = STYLED && a.bstyle && a.bstyle[b] == 1;
+        const float x = r / r0;
+        const bool stretched = fene && !(x < 1.f);
+        fene_bad = stretched ? pt | 0x80000000u : fene_bad;
+        const float cc = fene ? (stretched ? 0.f : -k / (1.f - x * x))
+                              : (r > 0.f ? -k * (r - r0) / r : 0.f);
         fx += cc * d[0];
         fy += cc * d[1];
         fz += cc * d[2];
     }
-    for (uint32_t e = e0; e < e1; ++e) {
+    if (STYLED && fene_bad) raise_err(a.err, DPDB_EPHYSICS, EW_FENE, tag, fene_bad & 0x7FFFFFFFu);
+    for (uint32_t e = e0; STYLED && e < e1; ++e) {
         const uint4 rec = a.arec[e];
         const uint32_t j1 = a.index_of_tag[rec.x], j2 = a.index_of_tag[rec.y];
         if (j1 >= a.n || j2 >= a.n) {
@@ -1323,7 +1326,7 @@ __global__ void k_bonds(BondArgs a) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.n) return;
     float fx, fy, fz;
-    if (!bond_force(a, i, fx, fy, fz)) return;
+    if (!bond_force<true>(a, i, fx, fy, fz)) return;
     a.f[0][i] += fx;
     a.f[1][i] += fy;
     a.f[2][i] += fz;

@@ -18,7 +18,12 @@ import paper_1311_0402_b200 as dpd  # noqa: E402
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 100
 
 
+ONLY = os.environ.get("CONFIGS")  # e.g. CONFIGS=C3,C4
+
+
 def run(name, L, n, params, run_cfg, chains=None):
+    if ONLY and name not in ONLY.split(","):
+        return
     box = dpd.SimBox((0.0, 0.0, 0.0), L)
     e = dpd.Engine(box, params, run_cfg, capacity=n)
     if chains:
