@@ -345,6 +345,16 @@ def run_b200(args, ws, rank, local):
     # setup, K steps with the per-step thermo read-back, download
     pinned = [torch.from_numpy(a).pin_memory().numpy() for a in state]
     out = [torch.empty(N_C3, dtype=torch.float64).pin_memory().numpy() for _ in range(6)]
+    def e2e_pass(k):
+        e.upload(dpd.ParticleStore.from_arrays(*pinned))
+        e.setup()
+        e.step_thermo(k)
+        if bricks:
+            e.download()
+        else:
+            e.download_state(out[0:3], out[3:6])
+
+    e2e_pass(args.warmup)  # untimed warm-up of the same path (first DMA into fresh pinned pages)
     barrier_sync(ws)
     t0 = time.perf_counter()
     e.upload(dpd.ParticleStore.from_arrays(*pinned))
