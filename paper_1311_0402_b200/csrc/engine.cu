@@ -98,6 +98,13 @@ struct dpdb_ctx {
     // per-step thermo (dpdb_step_thermo): block partials of the phase-2 pass
     // and the records, written by the device straight into mapped pinned memory
     double* thermo_part{};
+    // dpdb_step_thermo: the one-CTA record fold runs on th_stream, off the
+    // step's critical path; the producers alternate between two partial
+    // buffers (thermo_part <-> thermo_part2) so step s+1 never waits for it
+    double* thermo_part2{};
+    cudaStream_t th_stream = nullptr;
+    cudaEvent_t th_prod[2]{}, th_cons[2]{};
+    int th_idx = 0;
     double *thermo_host{}, *thermo_host_dev{};
     size_t thermo_cap = 0;  // records
     int64_t step = 0;
@@ -177,6 +184,7 @@ int dalloc(dpdb_ctx* ctx, T*& p, size_t count) {
 
 int check_device(dpdb_ctx* ctx) {
     CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->th_stream) CK(cudaStreamSynchronize(ctx->th_stream));
     DevErr e{};
     CK(cudaMemcpy(&e, ctx->err, sizeof e, cudaMemcpyDeviceToHost));
     if (!e.code) return 0;
@@ -814,8 +822,13 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
     if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&ctx->halo_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_pack, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming) != cudaSuccess)
+        cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->th_stream, cudaStreamNonBlocking) != cudaSuccess)
         return bail(fail(ctx, DPDB_EDEVICE, "cudaStreamCreate"));
+    for (int k = 0; k < 2; ++k)
+        if (cudaEventCreateWithFlags(&ctx->th_prod[k], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx->th_cons[k], cudaEventDisableTiming) != cudaSuccess)
+            return bail(fail(ctx, DPDB_EDEVICE, "cudaEventCreate"));
     ctx->cap = std::max<size_t>(capacity, 1);
     ctx->n_pad = (ctx->cap + 31) & ~(size_t)31;
     const size_t c = ctx->n_pad;
@@ -854,6 +867,7 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         (rc = dalloc(ctx, ctx->err, 1)) || (rc = dalloc(ctx, ctx->red, (size_t)RED_BLOCKS * 4)) ||
         (rc = dalloc(ctx, ctx->red_out, 16)) || (rc = dalloc(ctx, ctx->tmp_u32, c)) ||
         (rc = dalloc(ctx, ctx->thermo_part, 4 * (c / 256 + 1))) ||
+        (rc = dalloc(ctx, ctx->thermo_part2, 4 * (c / 256 + 1))) ||
         (rc = dalloc(ctx, ctx->blk_ghost, c / dpdb::FORCE_BLOCK + 1)))
         return bail(rc);
     ctx->md_list_cap = ctx->md_valid ? 8 * c : 1;  // a corner particle sits in 7 lists
@@ -915,7 +929,7 @@ int dpdb_destroy(dpdb_ctx* ctx) {
                     ctx->vel4, ctx->pos4n, ctx->vel4n, ctx->keys, ctx->keys2, ctx->vals, ctx->vals2, ctx->hist,
                     ctx->cell_start, ctx->ostart, ctx->rank_of_cell, ctx->stencil, ctx->stencil_n,
                     ctx->cell_flags, ctx->stencil_code, ctx->cell_lo, ctx->entries, ctx->counts, ctx->fwalk, ctx->rowmeta,
-                    ctx->err, ctx->red, ctx->red_out, ctx->thermo_part, ctx->blk_ghost, ctx->prof_acc,
+                    ctx->err, ctx->red, ctx->red_out, ctx->thermo_part, ctx->thermo_part2, ctx->blk_ghost, ctx->prof_acc,
                     ctx->tmp_u32, ctx->bond_off, ctx->bond_partner, ctx->index_of_tag,
                     ctx->bond_k, ctx->bond_r0, ctx->bond_style, ctx->ang_off, ctx->ang_rec, ctx->ang_k,
                     ctx->ang_t0, ctx->md_masks, ctx->md_mig, ctx->md_slot,
@@ -933,6 +947,14 @@ int dpdb_destroy(dpdb_ctx* ctx) {
     if (ctx->halo_stream) cudaStreamDestroy(ctx->halo_stream);
     if (ctx->ev_pack) cudaEventDestroy(ctx->ev_pack);
     if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
+    if (ctx->th_stream) {
+        cudaStreamSynchronize(ctx->th_stream);
+        cudaStreamDestroy(ctx->th_stream);
+    }
+    for (int k = 0; k < 2; ++k) {
+        if (ctx->th_prod[k]) cudaEventDestroy(ctx->th_prod[k]);
+        if (ctx->th_cons[k]) cudaEventDestroy(ctx->th_cons[k]);
+    }
     delete ctx;
     return 0;
 }
@@ -1525,10 +1547,18 @@ namespace {
 // the pass that applies phase 2 of step n also reduces its thermo partials
 // and k_thermo_final writes record n -- no host synchronisation per step.
 int thermo_record(dpdb_ctx* ctx, uint32_t nblocks, double* rec) {
-    dpdb::k_thermo_final<<<1, 256, 0, ctx->stream>>>(ctx->thermo_part, nblocks, (uint32_t)ctx->n,
-                                                      ctx->step, rec);
+    const int k = ctx->th_idx;
+    CK(cudaEventRecord(ctx->th_prod[k], ctx->stream));  // partials of this step written
+    CK(cudaStreamWaitEvent(ctx->th_stream, ctx->th_prod[k], 0));
+    dpdb::k_thermo_final<<<1, 256, 0, ctx->th_stream>>>(ctx->thermo_part, nblocks, (uint32_t)ctx->n,
+                                                         ctx->step, rec);
     CKL();
+    CK(cudaEventRecord(ctx->th_cons[k], ctx->th_stream));
     ctx->launches[ST_OTHER]++;
+    // the next producer writes the other buffer, once its previous fold is done
+    std::swap(ctx->thermo_part, ctx->thermo_part2);
+    ctx->th_idx = k ^ 1;
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->th_cons[k ^ 1], 0));
     return 0;
 }
 
