@@ -217,6 +217,26 @@ int check_device(dpdb_ctx* ctx) {
     return fail(ctx, e.code, msg);
 }
 
+// Per-step record fold off the critical path: the record kernel runs on
+// th_stream once the producer (force epilogue or k_integrate) has written its
+// block partials; the next producer writes the other partial buffer, after the
+// fold that last read it.
+template <class Launch>
+int thermo_fold(dpdb_ctx* ctx, Launch launch) {
+    const int k = ctx->th_idx;
+    CK(cudaEventRecord(ctx->th_prod[k], ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->th_stream, ctx->th_prod[k], 0));
+    launch(ctx->th_stream, ctx->thermo_part);
+    CKL();
+    CK(cudaEventRecord(ctx->th_cons[k], ctx->th_stream));
+    ctx->launches[ST_OTHER]++;
+    std::swap(ctx->thermo_part, ctx->thermo_part2);
+    ctx->th_idx = k ^ 1;
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->th_cons[k ^ 1], 0));
+    return 0;
+}
+
+
 void mark(dpdb_ctx* ctx, int stage) {
     if (!ctx->timing) return;
     if (ctx->ev_used == ctx->ev_pool.size()) {
@@ -1547,21 +1567,10 @@ namespace {
 // the pass that applies phase 2 of step n also reduces its thermo partials
 // and k_thermo_final writes record n -- no host synchronisation per step.
 int thermo_record(dpdb_ctx* ctx, uint32_t nblocks, double* rec) {
-    const int k = ctx->th_idx;
-    CK(cudaEventRecord(ctx->th_prod[k], ctx->stream));  // partials of this step written
-    CK(cudaStreamWaitEvent(ctx->th_stream, ctx->th_prod[k], 0));
-    dpdb::k_thermo_final<<<1, 256, 0, ctx->th_stream>>>(ctx->thermo_part, nblocks, (uint32_t)ctx->n,
-                                                         ctx->step, rec);
-    CKL();
-    CK(cudaEventRecord(ctx->th_cons[k], ctx->th_stream));
-    ctx->launches[ST_OTHER]++;
-    // the next producer writes the other buffer, once its previous fold is done
-    std::swap(ctx->thermo_part, ctx->thermo_part2);
-    ctx->th_idx = k ^ 1;
-    CK(cudaStreamWaitEvent(ctx->stream, ctx->th_cons[k ^ 1], 0));
-    return 0;
+    return thermo_fold(ctx, [&](cudaStream_t st, const double* part) {
+        dpdb::k_thermo_final<<<1, 256, 0, st>>>(part, nblocks, (uint32_t)ctx->n, ctx->step, rec);
+    });
 }
-
 int run_steps(dpdb_ctx* ctx, int64_t nsteps, double* rec = nullptr) {
     if (!ctx->have_table) return fail(ctx, DPDB_ECONFIG, "step: call dpdb_setup first");
     const bool th = rec != nullptr;

@@ -268,28 +268,6 @@ __global__ void __launch_bounds__(256) k_integrate(IntegrateArgs a) {
     }
 }
 
-// Brick runs: the raw per-brick sums {step, sum v_x, sum v_y, sum v_z,
-// sum |v|^2} of one step (combined across bricks in brick order by the host)
-__global__ void __launch_bounds__(256) k_thermo_sums(const double* part, uint32_t nblocks, int64_t step,
-                                                     double* rec) {
-    double v[4] = {0.0, 0.0, 0.0, 0.0};
-    for (uint32_t b = threadIdx.x; b < nblocks; b += 256)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) v[q] += part[4 * b + q];
-    __shared__ double tot[4];
-    block_sum4<256>(v, tot);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        rec[0] = (double)step;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) rec[1 + q] = tot[q];
-    }
-}
-
-// Per-step thermo record from the block partials of the pass that applied
-// phase 2 (fixed order): rec = {step, kT, P_x, P_y, P_z} with
-// kT = (sum |v|^2 - |sum v|^2 / n) / (3 n), the COM-subtracted temperature of
-// compute_temperature (src/core.cpp:141-149) in one pass.
 // Thread t folds partials t, t + 256, ... in that order; the loads of eight
 // consecutive ones are issued before their adds (a plain loop serialises one
 // memory latency per partial: ~10 us for 8192 partials).
@@ -313,6 +291,26 @@ __device__ __forceinline__ void fold_partials4(const double* part, uint32_t npar
     }
 }
 
+// Brick runs: the raw per-brick sums {step, sum v_x, sum v_y, sum v_z,
+// sum |v|^2} of one step (combined across bricks in brick order by the host)
+__global__ void __launch_bounds__(256) k_thermo_sums(const double* part, uint32_t nblocks, int64_t step,
+                                                     double* rec) {
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    fold_partials4(part, nblocks, v);
+    __shared__ double tot[4];
+    block_sum4<256>(v, tot);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        rec[0] = (double)step;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) rec[1 + q] = tot[q];
+    }
+}
+
+// Per-step thermo record from the block partials of the pass that applied
+// phase 2 (fixed order): rec = {step, kT, P_x, P_y, P_z} with
+// kT = (sum |v|^2 - |sum v|^2 / n) / (3 n), the COM-subtracted temperature of
+// compute_temperature (src/core.cpp:141-149) in one pass.
 __global__ void __launch_bounds__(256) k_thermo_final(const double* part, uint32_t nblocks, uint32_t n,
                                                       int64_t step, double* rec) {
     double v[4] = {0.0, 0.0, 0.0, 0.0};
