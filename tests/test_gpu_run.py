@@ -259,6 +259,38 @@ def test_step_thermo_records(monkeypatch, fuse):
     assert list(rec2["step"]) == [12, 13, 14]
 
 
+def test_step_thermo_long_call_and_interleaving():
+    """A call longer than the preallocated record ring (4096) grows it; the
+    side-stream record folds alternate between two partial buffers, so
+    records stay exact across interleaved dpdb_step / dpdb_thermo calls."""
+    box, obox, st = _sys.fluid((6, 6, 6), 3.0, seed=33)
+    a = _sys.engine(box, st, run=dpd.RunConfig(rebuild_every=5))
+    b = _sys.engine(box, st, run=dpd.RunConfig(rebuild_every=5))
+    a.setup()
+    b.setup()
+    rec = b.step_thermo(4101)
+    assert len(rec["step"]) == 4101 and rec["step"][0] == 1 and rec["step"][-1] == 4101
+    assert np.all(np.isfinite(rec["kbt"])) and abs(rec["kbt"][-100:].mean() - 1.0) < 0.1
+    a.step(4100)
+    a.step(1)
+    t = a.thermo()
+    assert t["step"] == 4101 and abs(rec["kbt"][-1] - t["kbt"]) <= 1e-12 * t["kbt"]
+    def one(e):
+        e.step(1)
+        return e.thermo()
+
+    for k in range(3):  # interleaved: step_thermo, step, thermo, step_thermo
+        r1 = b.step_thermo(2)
+        b.step(1)
+        t1 = b.thermo()
+        r2 = b.step_thermo(1)
+        ref = [one(a) for _ in range(4)]
+        got = [(r1["step"][0], r1["kbt"][0]), (r1["step"][1], r1["kbt"][1]),
+               (t1["step"], t1["kbt"]), (r2["step"][0], r2["kbt"][0])]
+        for (s_, kt), t in zip(got, ref):
+            assert s_ == t["step"] and abs(kt - t["kbt"]) <= 1e-12 * t["kbt"], (k, s_)
+
+
 @pytest.mark.parametrize("mode", [0, 1])
 def test_closed_box_walls(mode):
     """walls on every axis, ideal gas with a = gamma = sigma = 0:
