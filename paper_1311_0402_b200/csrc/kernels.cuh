@@ -428,13 +428,21 @@ __global__ void __launch_bounds__(256) k_scan_totals(uint32_t* __restrict__ tota
     totals[threadIdx.x] = t[threadIdx.x];
 }
 
+#ifndef DPDB_RS_BATCH
+#define DPDB_RS_BATCH 2
+#endif
+// Rounds of 256 keys are ranked RS_BATCH at a time: one barrier pair per batch
+// (the per-digit scan covers the batch's rounds in order), so the stable
+// order (tile, round, warp, lane) is unchanged.
 __global__ void __launch_bounds__(RS_THREADS) k_radix_downsweep(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
     uint32_t* __restrict__ vout, uint32_t n, int shift, uint32_t mask, uint32_t num_tiles,
     const uint32_t* __restrict__ offs, const uint32_t* __restrict__ digit_base) {
+    constexpr int RB = DPDB_RS_BATCH;
+    static_assert(RS_ITEMS % RB == 0, "batches must tile the rounds");
     __shared__ uint32_t s_base[256];
-    __shared__ uint32_t s_cnt[8][256];
-    __shared__ uint32_t s_pref[8][256];
+    __shared__ uint32_t s_cnt[RB][8][256];
+    __shared__ uint32_t s_pref[RB][8][256];
     const uint32_t tile = blockIdx.x;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t key[RS_ITEMS], val[RS_ITEMS];
@@ -446,34 +454,47 @@ __global__ void __launch_bounds__(RS_THREADS) k_radix_downsweep(
     }
     s_base[threadIdx.x] = offs[threadIdx.x * num_tiles + tile] + digit_base[threadIdx.x];
 #pragma unroll
-    for (int w = 0; w < 8; ++w) s_cnt[w][threadIdx.x] = 0;
+    for (int rr = 0; rr < RB; ++rr)
+#pragma unroll
+        for (int w = 0; w < 8; ++w) s_cnt[rr][w][threadIdx.x] = 0;
     __syncthreads();
     const uint32_t lt = lanemask_lt();
 #pragma unroll
-    for (int r = 0; r < RS_ITEMS; ++r) {
-        const uint32_t idx = tile * RS_TILE + r * RS_THREADS + threadIdx.x;
-        const bool valid = idx < n;
-        const uint32_t d = valid ? (key[r] >> shift) & mask : 256u + lane;
-        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
-        const uint32_t rank = __popc(peers & lt);
-        if (valid && (__ffs(peers) - 1) == (int)lane) s_cnt[warp][d] = __popc(peers);
+    for (int r0 = 0; r0 < RS_ITEMS; r0 += RB) {
+        uint32_t d[RB], rank[RB];
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr) {
+            const int r = r0 + rr;
+            const uint32_t idx = tile * RS_TILE + r * RS_THREADS + threadIdx.x;
+            const bool valid = idx < n;
+            d[rr] = valid ? (key[r] >> shift) & mask : 256u + lane;
+            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d[rr]);
+            rank[rr] = __popc(peers & lt);
+            if (valid && (__ffs(peers) - 1) == (int)lane) s_cnt[rr][warp][d[rr]] = __popc(peers);
+        }
         __syncthreads();
         {
             uint32_t run = s_base[threadIdx.x];
 #pragma unroll
-            for (int w = 0; w < 8; ++w) {
-                const uint32_t c = s_cnt[w][threadIdx.x];
-                s_pref[w][threadIdx.x] = run;
-                s_cnt[w][threadIdx.x] = 0;
-                run += c;
-            }
+            for (int rr = 0; rr < RB; ++rr)
+#pragma unroll
+                for (int w = 0; w < 8; ++w) {
+                    const uint32_t c = s_cnt[rr][w][threadIdx.x];
+                    s_pref[rr][w][threadIdx.x] = run;
+                    s_cnt[rr][w][threadIdx.x] = 0;
+                    run += c;
+                }
             s_base[threadIdx.x] = run;
         }
         __syncthreads();
-        if (valid) {
-            const uint32_t dst = s_pref[warp][d] + rank;
-            kout[dst] = key[r];
-            vout[dst] = val[r];
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr) {
+            const int r = r0 + rr;
+            if (d[rr] < 256u) {
+                const uint32_t dst = s_pref[rr][warp][d[rr]] + rank[rr];
+                kout[dst] = key[r];
+                vout[dst] = val[r];
+            }
         }
     }
 }
