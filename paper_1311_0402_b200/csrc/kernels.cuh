@@ -966,13 +966,16 @@ __device__ __forceinline__ float fsel(bool p, float a, float b) {
 }
 
 constexpr int RB_BLOCK = 32 * DPDB_FORCE_TPW * DPDB_FORCE_WARPS;  // == FORCE_BLOCK (force.cuh)
-constexpr int RB_THREADS = 256;
+#ifndef DPDB_RB_THREADS
+#define DPDB_RB_THREADS 256
+#endif
+constexpr int RB_THREADS = DPDB_RB_THREADS;  // lanes per CTA (RB_BLOCK / RB_THREADS passes)
 constexpr int RB_SLOTS = 29;     // 27 stencil cells + one split by the cut-out + a trash slot
 constexpr size_t RB_SMEM = (size_t)RB_SLOTS * RB_THREADS * 6 + RB_BLOCK * 4;
 constexpr uint32_t RB_NONE = 0xFFFFFFFFu;
 
 template <bool WALK, bool GH>
-__global__ void __launch_bounds__(RB_THREADS, 4) k_build_range(BuildArgs a) {
+__global__ void __launch_bounds__(RB_THREADS, 1024 / RB_THREADS) k_build_range(BuildArgs a) {
     extern __shared__ uint32_t rb_smem[];  // RB_SMEM bytes (dynamic: > 48 KB)
     uint32_t(*rs)[RB_THREADS] = reinterpret_cast<uint32_t(*)[RB_THREADS]>(rb_smem);
     uint16_t(*rl)[RB_THREADS] =
