@@ -121,6 +121,7 @@ def _declare(L):
                                          sz, sz, f64p, f64p, f64p, u32p, d, d, u,
                                          u32p, u16p, u16p, i]),
         "orc_join_core_skin": (None, [u, u, i, u32p, u16p, u16p]),
+        "orc_table_diff": (C.c_int64, [u, u, i, i, u32p, u16p, u16p, i, i, u32p, u16p, u16p, i]),
         "orc_tile_transpose": (None, [u, u, u32p]),
         "orc_params_make": (i, [C.c_int32, f64p, f64p, d, d, d, d, C.POINTER(Params)]),
         "orc_compute_forces": (i, [C.POINTER(Params), C.POINTER(Box), sz,
@@ -281,6 +282,19 @@ class OGrid:
                                              n_all, x, y, z, tag, r_c, skin, maxn, entries, core,
                                              skinc, nthreads))
         return entries.reshape(-1, maxn), core, skinc
+
+
+def table_diff(maxn, a, b, nthreads=8):
+    """First row where two tables differ (counts or entries through the
+    core_at / skin_at accessors), -1 when identical.  a, b: (tiled, joined,
+    entries, core, skin)."""
+    n = len(a[3])
+    assert len(b[3]) >= n
+    return int(lib().orc_table_diff(n, maxn, int(a[0]), int(a[1]),
+                                    np.ascontiguousarray(a[2]).reshape(-1), a[3], a[4],
+                                    int(b[0]), int(b[1]), np.ascontiguousarray(b[2]).reshape(-1),
+                                    np.ascontiguousarray(b[3][:n]), np.ascontiguousarray(b[4][:n]),
+                                    nthreads))
 
 
 def make_params(a=25.0, gamma=4.5, kbt=1.0, s=1.0, r_c=1.0, dt=0.01, n_species=1):

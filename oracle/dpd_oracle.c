@@ -659,6 +659,33 @@ int orc_build_neighbor_table(const orc_grid* g, const orc_box* box, const uint32
     return ORC_OK;
 }
 
+/* test helper (not a reference function): the core_at / skin_at accessors of
+ * inc/neighbor_table.hpp:33-39 applied to two tables in any layouts */
+static inline uint32_t tbl_skin_at(int tiled, int joined, uint32_t maxn, const uint32_t* e,
+                                   uint32_t nc, uint32_t i, uint32_t k) {
+    return e[orc_raw_index(tiled, maxn, i, joined ? nc + k : maxn - 1 - k)];
+}
+
+int64_t orc_table_diff(uint32_t n_rows, uint32_t maxn, int tiled_a, int joined_a,
+                       const uint32_t* ent_a, const uint16_t* core_a, const uint16_t* skin_a,
+                       int tiled_b, int joined_b, const uint32_t* ent_b, const uint16_t* core_b,
+                       const uint16_t* skin_b, int nthreads) {
+    int64_t first = INT64_MAX;
+    if (nthreads < 1) nthreads = 1;
+#pragma omp parallel for schedule(static, 4096) num_threads(nthreads) reduction(min : first)
+    for (int64_t ii = 0; ii < (int64_t)n_rows; ++ii) {
+        const uint32_t i = (uint32_t)ii;
+        int bad = core_a[i] != core_b[i] || skin_a[i] != skin_b[i];
+        for (uint32_t k = 0; !bad && k < core_a[i]; ++k)
+            bad = ent_a[orc_raw_index(tiled_a, maxn, i, k)] != ent_b[orc_raw_index(tiled_b, maxn, i, k)];
+        for (uint32_t k = 0; !bad && k < skin_a[i]; ++k)
+            bad = tbl_skin_at(tiled_a, joined_a, maxn, ent_a, core_a[i], i, k) !=
+                  tbl_skin_at(tiled_b, joined_b, maxn, ent_b, core_b[i], i, k);
+        if (bad && ii < first) first = ii;
+    }
+    return first == INT64_MAX ? -1 : first;
+}
+
 /* core asc then skin asc, counts kept (core_count, skin_count) */
 void orc_join_core_skin(uint32_t n_rows, uint32_t maxn, int tiled, uint32_t* entries,
                         uint16_t* core, uint16_t* skinc) {

@@ -119,6 +119,13 @@ void orc_join_core_skin(uint32_t n_rows, uint32_t maxn, int tiled, uint32_t* ent
                         uint16_t* core, uint16_t* skinc);
 void orc_tile_transpose(uint32_t n_rows_pad, uint32_t maxn, uint32_t* entries);
 size_t orc_raw_index(int tiled, uint32_t maxn, uint32_t i, uint32_t k);
+/* test helper: compare table A (any layout) with table B (any layout) row by
+ * row through the inc/neighbor_table.hpp:33-39 accessors; returns the first
+ * differing row (counts or any core/skin entry), or -1 when identical */
+int64_t orc_table_diff(uint32_t n_rows, uint32_t maxn, int tiled_a, int joined_a,
+                       const uint32_t* ent_a, const uint16_t* core_a, const uint16_t* skin_a,
+                       int tiled_b, int joined_b, const uint32_t* ent_b, const uint16_t* core_b,
+                       const uint16_t* skin_b, int nthreads);
 
 /* ------------------------------------------------------------------ forces */
 typedef struct {

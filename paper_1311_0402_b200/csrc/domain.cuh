@@ -216,7 +216,9 @@ struct UnpackArgs {
     uint32_t* vals;
     const uint32_t* slot_of;  // update: receive index -> ghost slot
     float4* pos4;
+    int4* posq;
     float4* vel4;
+    PosQ pq;
     DevGrid grid;
     uint32_t base;       // first slot (n for ghosts, n_keep for migrants)
     uint32_t count;
@@ -289,6 +291,7 @@ __global__ void k_unpack(UnpackArgs a, const void* in) {
         a.pos4[g] = make_float4((float)(rec.x[0] - a.grid.centre[0]),
                                 (float)(rec.x[1] - a.grid.centre[1]),
                                 (float)(rec.x[2] - a.grid.centre[2]), __uint_as_float(tw));
+        a.posq[g] = posq_of(a.pq, rec.x[0], rec.x[1], rec.x[2], tw);
         a.vel4[g] = make_float4((float)rec.v[0], (float)rec.v[1], (float)rec.v[2],
                                 __uint_as_float(sig));
     }

@@ -60,7 +60,8 @@ struct dpdb_ctx {
     float *f[3]{}, *f2[3]{};
     uint32_t *tag{}, *tag2{}, *mol{}, *mol2{};
     uint8_t *sp{}, *sp2{};
-    float4 *pos4{}, *vel4{}, *pos4n{}, *vel4n{};  // n: next-step streams of the fused force pass
+    float4 *pos4{}, *vel4{}, *vel4n{};  // n: next-step streams of the fused force pass
+    int4 *posq{}, *posqn{};  // pair-force frame (PosQ) + the fused pass's next-step buffer
     uint32_t *keys{}, *keys2{}, *vals{}, *vals2{}, *hist{};
     uint32_t *cell_start{}, *ostart{}, *rank_of_cell{}, *stencil{};
     uint8_t *stencil_n{}, *cell_flags{}, *stencil_code{};
@@ -282,6 +283,31 @@ dpdb::BoundaryArgs boundary(const dpdb_ctx* ctx) {
     return b;
 }
 
+// The pair-force frame (dpdb::PosQ, kernels.cuh): wrap axes map the slab
+// [lo, lo + L) onto the whole int32 circle; other axes use the largest power
+// of two that keeps |x - centre| <= L/2 + ghost layers + a margin in range.
+// qs: length per quantum (fp32), what the force kernels multiply by.
+dpdb::PosQ posq_frame(const dpdb_ctx* ctx, float qs[3]) {
+    dpdb::PosQ q{};
+    const HostGrid& g = ctx->grid;
+    for (int k = 0; k < 3; ++k) {
+        const double len = g.slab_hi[k] - g.slab_lo[k];
+        q.wrap[k] = g.wrap[k] ? 1 : 0;
+        if (q.wrap[k]) {
+            q.org[k] = g.slab_lo[k];
+            q.s[k] = 4294967296.0 / len;
+            if (qs) qs[k] = (float)(len / 4294967296.0);
+        } else {
+            const double half = 0.5 * len + 2.0 * (ctx->params.r_c + ctx->run.skin) + 16.0;
+            const int e = (int)std::floor(std::log2(2147483647.0 / half));
+            q.org[k] = 0.5 * (g.slab_lo[k] + g.slab_hi[k]);
+            q.s[k] = std::ldexp(1.0, e);
+            if (qs) qs[k] = std::ldexp(1.0f, -e);
+        }
+    }
+    return q;
+}
+
 // fp32 wrap lengths of the single-domain slab (wrapmode axes)
 void wrap_lengths(const dpdb_ctx* ctx, float L[3], float H[3]) {
     for (int k = 0; k < 3; ++k) {
@@ -305,7 +331,9 @@ dpdb::IntegrateArgs integrate_args(dpdb_ctx* ctx, bool defer_wrap) {
     a.tag = ctx->tag;
     a.sp = ctx->multi ? ctx->sp : nullptr;
     a.pos4 = ctx->pos4;
+    a.posq = ctx->posq;
     a.vel4 = ctx->vel4;
+    a.pq = posq_frame(ctx, nullptr);
     a.keys = ctx->keys;
     a.vals = ctx->vals;
     a.err = ctx->err;
@@ -404,7 +432,9 @@ int do_permute(dpdb_ctx* ctx, bool forces) {
     a.cell_start = ctx->cell_start;
     a.ostart = ctx->ostart;
     a.pos4 = ctx->pos4;
+    a.posq = ctx->posq;
     a.vel4 = ctx->vel4;
+    a.pq = posq_frame(ctx, nullptr);
     a.n = (uint32_t)ctx->n;
     a.n_total_cells = ctx->grid.n_total_cells;
     a.key_shift = 3 * ctx->grid.sub_bits;
@@ -522,8 +552,9 @@ int do_streams(dpdb_ctx* ctx, uint32_t* sig_out) {
     const HostGrid& g = ctx->grid;
     dpdb::k_streams<<<blocks_for(ctx->n, 256), 256, 0, ctx->stream>>>(
         ctx->x[0], ctx->x[1], ctx->x[2], ctx->v[0], ctx->v[1], ctx->v[2], ctx->tag,
-        ctx->multi ? ctx->sp : nullptr, ctx->pos4, ctx->vel4, sig_out, (g.slab_lo[0] + g.slab_hi[0]) / 2, (g.slab_lo[1] + g.slab_hi[1]) / 2,
-        (g.slab_lo[2] + g.slab_hi[2]) / 2, (uint32_t)ctx->n);
+        ctx->multi ? ctx->sp : nullptr, ctx->pos4, ctx->posq, ctx->vel4, sig_out,
+        (g.slab_lo[0] + g.slab_hi[0]) / 2, (g.slab_lo[1] + g.slab_hi[1]) / 2, (g.slab_lo[2] + g.slab_hi[2]) / 2,
+        posq_frame(ctx, nullptr), (uint32_t)ctx->n);
     CKL();
     ctx->launches[ST_OTHER]++;
     return 0;
@@ -588,12 +619,9 @@ dpdb::BondArgs bond_args(dpdb_ctx* ctx) {
     b.ak = ctx->ang_k;
     b.at0 = ctx->ang_t0;
     b.index_of_tag = ctx->index_of_tag;
-    b.pos4 = ctx->pos4;
-    for (int k = 0; k < 3; ++k) {
-        b.f[k] = ctx->f[k];
-        b.periodic[k] = ctx->box.periodic[k];
-    }
-    wrap_lengths(ctx, b.L, b.H);
+    b.posq = ctx->posq;
+    for (int k = 0; k < 3; ++k) b.f[k] = ctx->f[k];
+    posq_frame(ctx, b.qs);
     b.err = ctx->err;
     b.n = (uint32_t)ctx->n;
     b.max_tag = ctx->max_tag;
@@ -609,7 +637,7 @@ int do_forces(dpdb_ctx* ctx, uint32_t step, int fuse = dpdb::FUSE_NONE, bool the
     if (!ctx->n) return 0;
     const dpdb_params& p = ctx->params;
     dpdb::ForceArgs a{};
-    a.pos4 = ctx->pos4;
+    a.posq = ctx->posq;
     a.vel4 = ctx->vel4;
     a.entries = ctx->entries;
     a.counts = ctx->counts;
@@ -625,8 +653,13 @@ int do_forces(dpdb_ctx* ctx, uint32_t step, int fuse = dpdb::FUSE_NONE, bool the
     a.a = (float)p.a[0];
     a.gamma = (float)p.gamma[0];
     a.sigma_dt = (float)(ctx->sigma[0] / std::sqrt(p.dt));
-    wrap_lengths(ctx, a.L, a.H);
-    for (int k = 0; k < 3; ++k) a.iL[k] = 1.0f / a.L[k];
+    posq_frame(ctx, a.qs);
+    for (int k = 0; k < 3; ++k) {
+        a.xd[k] = ctx->x[k];
+        const double len = ctx->grid.slab_hi[k] - ctx->grid.slab_lo[k];
+        a.Lw[k] = ctx->grid.wrap[k] ? len : 0.0;
+        a.iLw[k] = ctx->grid.wrap[k] ? 1.0 / len : 0.0;
+    }
     const bool body = ctx->run.body_force != 0.0;
     a.body_g = (float)ctx->run.body_force;
     a.drive_axis = ctx->run.drive_axis;
@@ -652,8 +685,11 @@ int do_forces(dpdb_ctx* ctx, uint32_t step, int fuse = dpdb::FUSE_NONE, bool the
     }
     if (fuse != dpdb::FUSE_NONE) {
         a.ia = integrate_args(ctx, defer_wrap);
+        // x(n+1) goes to the second buffer: close pairs of other blocks read x(n)
+        // through a.xd while this launch runs (the caller swaps x / x2 after it)
+        for (int k = 0; k < 3; ++k) a.ia.x[k] = ctx->x2[k];
         if (thermo) a.ia.thermo_part = ctx->thermo_part;
-        a.pos4n = ctx->pos4n;
+        a.posqn = ctx->posqn;
         a.vel4n = ctx->vel4n;
     }
     if (ctx->multi || a.smode != 1 || a.has_bonds)  // bonds: in the GENERAL epilogue
@@ -864,7 +900,8 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         (rc = dalloc(ctx, ctx->sp, c)) || (rc = dalloc(ctx, ctx->sp2, c)) ||
         (rc = dalloc(ctx, ctx->mol, c)) || (rc = dalloc(ctx, ctx->mol2, c)) ||
         (rc = dalloc(ctx, ctx->pos4, c)) || (rc = dalloc(ctx, ctx->vel4, c)) ||
-        (rc = dalloc(ctx, ctx->pos4n, c)) || (rc = dalloc(ctx, ctx->vel4n, c)) ||
+        (rc = dalloc(ctx, ctx->posq, c)) || (rc = dalloc(ctx, ctx->posqn, c)) ||
+        (rc = dalloc(ctx, ctx->vel4n, c)) ||
         (rc = dalloc(ctx, ctx->keys, c)) || (rc = dalloc(ctx, ctx->keys2, c)) ||
         (rc = dalloc(ctx, ctx->vals, c)) || (rc = dalloc(ctx, ctx->vals2, c)) ||
         (rc = dalloc(ctx, ctx->hist, std::max<size_t>((size_t)256 * tiles + 256,
@@ -946,7 +983,7 @@ int dpdb_destroy(dpdb_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     md_release(ctx);
     void* ptrs[] = {ctx->tag, ctx->tag2, ctx->mol, ctx->mol2, ctx->sp, ctx->sp2, ctx->pos4,
-                    ctx->vel4, ctx->pos4n, ctx->vel4n, ctx->keys, ctx->keys2, ctx->vals, ctx->vals2, ctx->hist,
+                    ctx->vel4, ctx->posq, ctx->posqn, ctx->vel4n, ctx->keys, ctx->keys2, ctx->vals, ctx->vals2, ctx->hist,
                     ctx->cell_start, ctx->ostart, ctx->rank_of_cell, ctx->stencil, ctx->stencil_n,
                     ctx->cell_flags, ctx->stencil_code, ctx->cell_lo, ctx->entries, ctx->counts, ctx->fwalk, ctx->rowmeta,
                     ctx->err, ctx->red, ctx->red_out, ctx->thermo_part, ctx->thermo_part2, ctx->blk_ghost, ctx->prof_acc,
@@ -1610,8 +1647,10 @@ int run_steps(dpdb_ctx* ctx, int64_t nsteps, double* rec = nullptr) {
         const bool next_rebuild = (ctx->step + 1) % ctx->run.rebuild_every == 0;
         TRY(do_forces(ctx, (uint32_t)ctx->step,
                       fuse ? (next_rebuild ? dpdb::FUSE_KEYS : dpdb::FUSE_STREAMS) : dpdb::FUSE_NONE, th));
-        if (fuse && !next_rebuild) {
-            std::swap(ctx->pos4, ctx->pos4n);
+        if (fuse)
+            for (int k = 0; k < 3; ++k) std::swap(ctx->x[k], ctx->x2[k]);
+        if (fuse && !next_rebuild) {  // pos4 is not written: the builder reads it after a permute
+            std::swap(ctx->posq, ctx->posqn);
             std::swap(ctx->vel4, ctx->vel4n);
         }
         integrated = fuse;
@@ -1756,6 +1795,7 @@ int dpdb_rdf(dpdb_ctx* ctx, uint32_t nbins, double rmax, uint64_t* hist) {
     if (!(rmax > 0) || rmax > ctx->params.r_c + ctx->run.skin + 1e-12)
         return fail(ctx, DPDB_ECONFIG, "rdf: 0 < rmax <= r_c + skin (the table's reach)");
     if (ctx->walk == 1 || ctx->walk == 2) TRY(unwalk(ctx));  // lane/ballot walk orders: back to reference rows
+    TRY(do_streams(ctx, nullptr));  // pos4 of the current state (the fused loop writes posq only)
     unsigned long long* d = reinterpret_cast<unsigned long long*>(ctx->tmp_u32);
     if ((size_t)nbins * 2 > ctx->n_pad) return fail(ctx, DPDB_ECONFIG, "rdf: more bins than scratch");
     CK(cudaMemsetAsync(d, 0, nbins * sizeof(unsigned long long), ctx->stream));

@@ -7,7 +7,7 @@
 #include <type_traits>
 
 struct ForceArgs {
-    const float4* pos4;
+    const int4* posq;   // fixed-point positions | tag word (PosQ, kernels.cuh)
     const float4* vel4;
     const uint32_t* entries;
     const uint32_t* counts;
@@ -19,8 +19,11 @@ struct ForceArgs {
     uint32_t step_mix;
     float rc2, inv_rc;
     float a, gamma, sigma_dt;  // single species: a, gamma, sigma / sqrt(dt)
-    float L[3], H[3];
-    float iL[3];  // 1 / L (fp32)
+    float qs[3];        // length per posq quantum, per axis
+    // close pairs (r < CLOSE_R): the pair vector again from the fp64 master
+    // coordinates (a posq quantum of 4e-8 is still 4e-5 of a 1e-3 separation)
+    const double* xd[3];
+    double Lw[3], iLw[3];  // wrap lengths (0: no wrap on that axis) and inverses
     float body_g;
     int drive_axis;
     double body_mid64;
@@ -30,10 +33,10 @@ struct ForceArgs {
     float ta[16], tg[16], ts[16];  // a_ij, gamma_ij, sigma_ij / sqrt(dt)
     // k_force_walk<.., FUSE>: the next Verlet pass (phase 2 of this step +
     // phase 1 of the next) runs in the epilogue on the block's fresh forces;
-    // streams go to pos4n / vel4n (the other buffer: neighbors still read this
+    // streams go to posqn / vel4n (the other buffer: neighbors still read this
     // step's), keys to ia.keys / ia.vals when the next step rebuilds.
     IntegrateArgs ia;
-    float4* pos4n;
+    int4* posqn;
     float4* vel4n;
     // bricks: run only the blocks with blk_sel[block] == sel_val (interior /
     // boundary split around the ghost update); null = every block
@@ -91,12 +94,34 @@ __device__ __forceinline__ float gaussian_hot(uint32_t ua, uint32_t ub) {
 
 __device__ __forceinline__ float gaussian_pair(uint32_t ua, uint32_t ub) { return gaussian_hot(ua, ub); }
 
-// Branch-free fp32 minimum image for the walk force kernel: L = 0 (and
-// invL = 0) on axes without wrap.  d - L*rint(d/L) equals min_image_f's
-// d -/+ L exactly (one rounding) whenever |d| is not within an ulp of L/2,
-// i.e. for every pair that can be within r_c.
-__device__ __forceinline__ float min_image_rint(float d, float L, float invL) {
-    return fmaf(-L, rintf(d * invL), d);
+// Pair vector in the posq frame: exact int32 difference (the minimum image on
+// wrap axes), one rounding to fp32.
+__device__ __forceinline__ void posq_delta(const ForceArgs& a, const int4& p, const int4& q, float& dx,
+                                           float& dy, float& dz) {
+    dx = (float)(p.x - q.x) * a.qs[0];
+    dy = (float)(p.y - q.y) * a.qs[1];
+    dz = (float)(p.z - q.z) * a.qs[2];
+}
+
+// r^2 below which the pair vector is re-formed from the fp64 master state
+// (r < 0.05: the posq quantum, <= 4.2e-8 up to L = 180, is then < 1.2e-6 of r;
+// about 1 pair in 8000 takes this branch)
+constexpr float CLOSE_R2 = 0.0025f;
+
+// The fp64 pair vector of the oracle (S:434-442 with src/core.cpp:129-139's
+// minimum image on wrap axes), rounded once to fp32; rare, so divergent.
+__device__ __forceinline__ float close_delta(const ForceArgs& a, uint32_t i, uint32_t j, float& dx, float& dy,
+                                             float& dz) {
+    double d[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        d[k] = __dsub_rn(a.xd[k][i], a.xd[k][j]);
+        if (a.Lw[k] > 0.0) d[k] = __dsub_rn(d[k], __dmul_rn(a.Lw[k], rint(__dmul_rn(d[k], a.iLw[k]))));
+    }
+    dx = (float)d[0];
+    dy = (float)d[1];
+    dz = (float)d[2];
+    return fmaf(dx, dx, fmaf(dy, dy, dz * dz));
 }
 
 __device__ __forceinline__ float weight_pow_f(float w, float s, int mode) {
@@ -116,6 +141,29 @@ constexpr int FQ = 64;  // per-warp pair queue (slots)
 // the order in which lanes or warps deliver their shares.
 constexpr float FIX_SCALE = 262144.0f;
 constexpr float FIX_INV = 1.0f / 262144.0f;
+
+// The C + D + R force of one pair as fixed-point shares
+// q = rint(F * 2^18) of F_ij = mag * r_ij.  Every product and sum is pinned
+// (explicit fmaf / __fmul_rn: the compiler may not pick a contraction), so
+// all pair kernels -- k_force and k_force_walk, fused or not -- give identical
+// bits for the same pair.
+template <bool GENERAL>
+__device__ __forceinline__ void pair_shares(float dx, float dy, float dz, float r2, const float4& vo,
+                                            const float4& vj, float xi, float ca, float cg, float cs,
+                                            float inv_rc, float s_exp, int smode, int& qx, int& qy,
+                                            int& qz) {
+    const float rinv = rsqrt_ftz(r2);
+    const float w = fmaxf(fmaf(__fmul_rn(-r2, rinv), inv_rc, 1.f), 0.f);
+    const float wr = GENERAL ? weight_pow_f(w, s_exp, smode) : w;
+    const float dvx = __fsub_rn(vo.x, vj.x), dvy = __fsub_rn(vo.y, vj.y), dvz = __fsub_rn(vo.z, vj.z);
+    const float ev = __fmul_rn(fmaf(dz, dvz, fmaf(dy, dvy, __fmul_rn(dx, dvx))), rinv);
+    const float fr = __fmul_rn(__fmul_rn(cs, wr), xi);                       // random
+    const float fd = fmaf(-__fmul_rn(cg, __fmul_rn(wr, wr)), ev, fr);        // - dissipative
+    const float mag = __fmul_rn(fmaf(ca, w, fd), __fmul_rn(rinv, FIX_SCALE));  // + conservative
+    qx = __float2int_rn(__fmul_rn(mag, dx));
+    qy = __float2int_rn(__fmul_rn(mag, dy));
+    qz = __float2int_rn(__fmul_rn(mag, dz));
+}
 
 // Offset of row position m of lane `lane` in its 32-row tile (raw_index,
 // inc/neighbor_table.hpp:27-31), relative to entries + i0*maxn + lane.
@@ -150,12 +198,12 @@ __device__ __forceinline__ uint32_t row_offset(uint32_t lane, uint32_t m, uint32
 // skin entries tagged with bit 31), so the in-block j < i entries are never
 // loaded.
 //
-// GENERAL: any weight exponent s and n_species > 1 (pos4.w = tag |
+// GENERAL: any weight exponent s and n_species > 1 (posq.w = tag |
 // species << 28, C/D/R coefficients from the ns x ns tables of PairParams,
 // inc/core.hpp:51-68).  !GENERAL is the single-species s = 1 fast path.
 template <bool GENERAL, bool TILED, bool JOINED, bool BODY, bool WALK>
 __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(ForceArgs a) {
-    __shared__ float4 q_d[FORCE_WARPS][FQ];   // (dx, dy, dz, tag_j)
+    __shared__ float4 q_d[FORCE_WARPS][FQ];   // (dx, dy, dz, tag_j) in the posq frame
     __shared__ uint32_t q_j[FORCE_WARPS][FQ]; // j | in_block << 26 | owner lane << 27
     __shared__ float4 own_v[FORCE_WARPS][32];
     __shared__ uint32_t own_t[FORCE_WARPS][32];
@@ -178,18 +226,19 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(ForceArgs a) {
         const uint32_t il = il0 + lane;  // my index in the block
         const uint32_t i = b0 + il;
         const bool live = il < bn;
-        float4 pi = make_float4(0.f, 0.f, 0.f, 0.f), vi = pi;
+        int4 pi = make_int4(0, 0, 0, 0);
+        float4 vi = make_float4(0.f, 0.f, 0.f, 0.f);
         uint32_t c = 0;
         if (live) {
-            pi = a.pos4[i];
+            pi = a.posq[i];
             vi = a.vel4[i];
             c = WALK ? a.fwalk[i] : a.counts[i];
         }
         own_v[warp][lane] = vi;
-        const uint32_t nc = WALK ? 0u : c & 0x1FFFu, fl = c >> 26;
+        const uint32_t nc = WALK ? 0u : c & 0x1FFFu;
         const uint32_t tot = WALK ? (c & 0x1FFFu) : nc + ((c >> 13) & 0x1FFFu);
         const uint32_t maxtot = __reduce_max_sync(0xFFFFFFFFu, tot);
-        const uint32_t tag_me = __float_as_uint(pi.w);
+        const uint32_t tag_me = (uint32_t)pi.w;
         own_t[warp][lane] = tag_me;
         uint32_t qhead = 0, qtail = 0;
         __syncwarp();
@@ -198,11 +247,18 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(ForceArgs a) {
             __syncwarp();
             const uint32_t s = (h + lane) & (FQ - 1);
             if ((uint32_t)lane < cnt) {
-                const float4 d = q_d[warp][s];
+                const float4 d4 = q_d[warp][s];
                 const uint32_t jj = q_j[warp][s];
                 const uint32_t o = jj >> 27, j = jj & 0x03FFFFFFu;
                 const float4 vo = own_v[warp][o];
-                uint32_t tag_i = own_t[warp][o], tag_j = __float_as_uint(d.w);
+                float dx = d4.x, dy = d4.y, dz = d4.z;
+                float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                if (r2 < CLOSE_R2) r2 = close_delta(a, b0 + il0 + o, j, dx, dy, dz);
+                if (r2 == 0.f) {
+                    coincident = true;
+                    bad_tag = own_t[warp][o];
+                }
+                uint32_t tag_i = own_t[warp][o], tag_j = __float_as_uint(d4.w);
                 float ca = a.a, cg = a.gamma, cs = a.sigma_dt;
                 if (GENERAL && a.ns > 1) {  // species ride in the top 4 bits of the tag word
                     const uint32_t q = (tag_i >> 28) * a.ns + (tag_j >> 28);
@@ -220,17 +276,9 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(ForceArgs a) {
                 uint32_t u1 = (ifirst ? sig_j : sig_i) ^ a.step_mix;
                 tea4(u0, u1);
                 const float xi = gaussian_pair(u0, u1);
-                const float r2 = fmaf(d.x, d.x, fmaf(d.y, d.y, d.z * d.z));
-                const float rinv = rsqrt_ftz(r2);
-                const float w = fmaxf(fmaf(-r2 * rinv, a.inv_rc, 1.f), 0.f);
-                const float wr = GENERAL ? weight_pow_f(w, a.s_exp, a.smode) : w;
-                const float ev =
-                    (d.x * (vo.x - vj.x) + d.y * (vo.y - vj.y) + d.z * (vo.z - vj.z)) * rinv;
-                const float mag =
-                    (ca * w - cg * (wr * wr) * ev + cs * wr * xi) * (rinv * FIX_SCALE);
-                const int qx = __float2int_rn(mag * d.x);
-                const int qy = __float2int_rn(mag * d.y);
-                const int qz = __float2int_rn(mag * d.z);
+                int qx, qy, qz;
+                pair_shares<GENERAL>(dx, dy, dz, r2, vo, vj, xi, ca, cg, cs, a.inv_rc, a.s_exp, a.smode,
+                                     qx, qy, qz);
                 int* ai = acc + 3 * (il0 + o);
                 atomicAdd(ai + 0, qx);
                 atomicAdd(ai + 1, qy);
@@ -253,34 +301,26 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(ForceArgs a) {
         if (0 < tot) e0 = __ldg(erow + row_offset<TILED, JN>(lane, 0, nc, maxn)) & EMASK;
         if (1 < tot) e1 = __ldg(erow + row_offset<TILED, JN>(lane, 1, nc, maxn)) & EMASK;
         if (2 < tot) e2 = __ldg(erow + row_offset<TILED, JN>(lane, 2, nc, maxn)) & EMASK;
-        float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (0 < tot) p0 = __ldg(a.pos4 + e0);
+        int4 p0 = make_int4(0, 0, 0, 0);
+        if (0 < tot) p0 = __ldg(a.posq + e0);
         for (uint32_t m = 0; m < maxtot; ++m) {
             const uint32_t j = e0;
-            const float4 pj = p0;
+            const int4 pj = p0;
             const uint32_t jl = j - b0;
             const bool inblk = jl < bn;
             const bool act = m < tot && (WALK || !(inblk && jl < il));  // lower index takes it
             e0 = e1;
             e1 = e2;
             if (m + 3 < tot) e2 = __ldg(erow + row_offset<TILED, JN>(lane, m + 3, nc, maxn)) & EMASK;
-            if (m + 1 < tot) p0 = __ldg(a.pos4 + e0);
-            float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
-            if (fl) {
-                if (fl & 1u) dx = min_image_f(dx, a.L[0], a.H[0]);
-                if (fl & 2u) dy = min_image_f(dy, a.L[1], a.H[1]);
-                if (fl & 4u) dz = min_image_f(dz, a.L[2], a.H[2]);
-            }
+            if (m + 1 < tot) p0 = __ldg(a.posq + e0);
+            float dx, dy, dz;
+            posq_delta(a, pi, pj, dx, dy, dz);
             const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-            if (act && r2 == 0.f) {
-                coincident = true;
-                bad_tag = tag_me;
-            }
-            const bool hit = act && r2 <= a.rc2 && r2 > 0.f;
+            const bool hit = act && r2 <= a.rc2;
             const uint32_t bal = __ballot_sync(0xFFFFFFFFu, hit);
             if (hit) {
                 const uint32_t s = (qtail + __popc(bal & lt)) & (FQ - 1);
-                q_d[warp][s] = make_float4(dx, dy, dz, pj.w);
+                q_d[warp][s] = make_float4(dx, dy, dz, __int_as_float(pj.w));
                 q_j[warp][s] = j | ((uint32_t)inblk << 26) | ((uint32_t)lane << 27);
             }
             qtail += __popc(bal);
@@ -320,10 +360,10 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(ForceArgs a) {
 // the hardware allows -- ~27 candidates are filtered per particle but only ~8
 // pairs evaluated, so phase A dominates the instruction count.
 //
-// Phase A (per candidate, per lane = row): one row-entry load and one pos4
+// Phase A (per candidate, per lane = row): one row-entry load and one posq
 // load, fp32 distance, |r| <= r_c, a ballot, and one 4-byte shared store of
 // j | lane << 27 into the warp's pair queue.  Everything else the pair needs
-// (d, tags, in-block test, min-image) is recomputed in phase B, which runs
+// (d, tags, in-block test) is recomputed in phase B, which runs
 // with all 32 lanes busy.  Row entries are fetched one group of 4 ahead with
 // compile-time strides (MAXN) and the 4 candidate positions of a group are
 // issued back to back, so each warp keeps up to 8 loads in flight without a
@@ -352,9 +392,8 @@ template <bool GENERAL, bool BODY, int MAXN, int FUSE>
 __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceArgs a) {
     static_assert(FORCE_TPW % 2 == 0, "tiles are dealt in snake order, two per round");
     __shared__ uint32_t q_j[FORCE_WARPS][FW_Q];  // j | owner lane << 27
-    __shared__ float4 own_p[FORCE_WARPS][32];
+    __shared__ int4 own_p[FORCE_WARPS][32];
     __shared__ float4 own_v[FORCE_WARPS][32];
-    __shared__ uint32_t own_fl[FORCE_WARPS][32];
     __shared__ int acc[FORCE_BLOCK * 3];
     if (a.blk_sel && a.blk_sel[blockIdx.x] != a.sel_val) return;  // whole CTA
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -376,19 +415,18 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceA
         if (il0 >= bn) continue;
         const uint32_t il = il0 + lane;
         const bool live = il < bn;
-        float4 pi = make_float4(0.f, 0.f, 0.f, 0.f), vi = pi;
+        int4 pi = make_int4(0, 0, 0, 0);
+        float4 vi = make_float4(0.f, 0.f, 0.f, 0.f);
         uint32_t c = 0;
         if (live) {
-            pi = a.pos4[b0 + il];
+            pi = a.posq[b0 + il];
             vi = a.vel4[b0 + il];
             c = a.fwalk[b0 + il];
         }
-        const uint32_t tot = c & 0x1FFFu, fl = c >> 26;
+        const uint32_t tot = c & 0x1FFFu;
         own_p[warp][lane] = pi;
         own_v[warp][lane] = vi;
-        own_fl[warp][lane] = fl;
         const uint32_t maxtot = __reduce_max_sync(0xFFFFFFFFu, tot);
-        const bool anywrap = __any_sync(0xFFFFFFFFu, fl != 0u);
         __syncwarp();
         uint32_t qtail = 0;
 
@@ -396,18 +434,15 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceA
             if ((uint32_t)lane < cnt) {
                 const uint32_t jw = q_j[warp][h + lane];
                 const uint32_t o = jw >> 27, j = jw & 0x07FFFFFFu;
-                const float4 po = own_p[warp][o];
+                const int4 po = own_p[warp][o];
                 const float4 vo = own_v[warp][o];
-                const float4 pj = __ldg(a.pos4 + j);
+                const int4 pj = __ldg(a.posq + j);
                 const float4 vj = __ldg(a.vel4 + j);
-                float dx = po.x - pj.x, dy = po.y - pj.y, dz = po.z - pj.z;
-                if (anywrap) {
-                    const uint32_t f = own_fl[warp][o];
-                    dx = min_image_rint(dx, (f & 1u) ? a.L[0] : 0.f, (f & 1u) ? a.iL[0] : 0.f);
-                    dy = min_image_rint(dy, (f & 2u) ? a.L[1] : 0.f, (f & 2u) ? a.iL[1] : 0.f);
-                    dz = min_image_rint(dz, (f & 4u) ? a.L[2] : 0.f, (f & 4u) ? a.iL[2] : 0.f);
-                }
-                uint32_t tag_i = __float_as_uint(po.w), tag_j = __float_as_uint(pj.w);
+                float dx, dy, dz;
+                posq_delta(a, po, pj, dx, dy, dz);
+                float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                if (r2 < CLOSE_R2) r2 = close_delta(a, b0 + il0 + o, j, dx, dy, dz);
+                uint32_t tag_i = (uint32_t)po.w, tag_j = (uint32_t)pj.w;
                 float ca = a.a, cg = a.gamma, cs = a.sigma_dt;
                 if (GENERAL && a.ns > 1) {  // species ride in the top 4 bits of the tag word
                     const uint32_t q = (tag_i >> 28) * a.ns + (tag_j >> 28);
@@ -423,21 +458,13 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceA
                 uint32_t u1 = (ifirst ? sig_j : sig_i) ^ a.step_mix;
                 tea4(u0, u1);
                 const float xi = gaussian_pair(u0, u1);
-                const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
                 if (r2 == 0.f) {
                     coincident = true;
                     bad_tag = tag_i;
                 }
-                const float rinv = rsqrt_ftz(r2);
-                const float w = fmaxf(fmaf(-r2 * rinv, a.inv_rc, 1.f), 0.f);
-                const float wr = GENERAL ? weight_pow_f(w, a.s_exp, a.smode) : w;
-                const float ev =
-                    (dx * (vo.x - vj.x) + dy * (vo.y - vj.y) + dz * (vo.z - vj.z)) * rinv;
-                const float mag =
-                    (ca * w - cg * (wr * wr) * ev + cs * wr * xi) * (rinv * FIX_SCALE);
-                const int qx = __float2int_rn(mag * dx);
-                const int qy = __float2int_rn(mag * dy);
-                const int qz = __float2int_rn(mag * dz);
+                int qx, qy, qz;
+                pair_shares<GENERAL>(dx, dy, dz, r2, vo, vj, xi, ca, cg, cs, a.inv_rc, a.s_exp, a.smode,
+                                     qx, qy, qz);
                 int* ai = acc + 3 * (il0 + o);
                 atomicAdd(ai + 0, qx);
                 atomicAdd(ai + 1, qy);
@@ -457,83 +484,66 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceA
         // (+ one prefetch group), and every word of the entries array is a
         // valid particle index (zeroed at allocation, only indices written
         // since), so positions past a row's end are harmless in-bounds reads
-        // masked by m < tot.  pos4 is addressed as (e << 4) bytes in 32-bit
+        // masked by m < tot.  posq is addressed as (e << 4) bytes in 32-bit
         // arithmetic, which drops the walk layout's skin tag (bit 31).
         const uint32_t* ep = a.entries + (size_t)(b0 + il0) * maxn + lane;
-        const char* pb = reinterpret_cast<const char*>(a.pos4);
+        const char* pb = reinterpret_cast<const char*>(a.posq);
         const char* vb = reinterpret_cast<const char*>(a.vel4);
         uint32_t* qw = q_j[warp];
-        auto phase_a = [&](auto wrap_c) {
-            constexpr bool WRAP = decltype(wrap_c)::value;
-            float lx = 0.f, ly = 0.f, lz = 0.f, ilx = 0.f, ily = 0.f, ilz = 0.f;
-            if (WRAP) {
-                if (fl & 1u) lx = a.L[0], ilx = a.iL[0];
-                if (fl & 2u) ly = a.L[1], ily = a.iL[1];
-                if (fl & 4u) lz = a.L[2], ilz = a.iL[2];
+        const float rc2 = a.rc2;
+        // one group = 4 row positions: positions of the group's candidates,
+        // prefetch of the next group's entries, filter, enqueue, drain
+        auto group = [&](uint32_t m0, const uint32_t (&cur)[4], uint32_t (&nxt)[4]) {
+            // lanes past their row end load the block's first particle
+            // instead (one shared line, no extra wavefronts); hit masks them
+            int4 p[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t jk = (FW_UNCOND || m0 + k < tot) ? cur[k] : b0;
+                p[k] = __ldg(reinterpret_cast<const int4*>(pb + (jk << 4)));
             }
-            const float rc2 = a.rc2;
-            // one group = 4 row positions: positions of the group's candidates,
-            // prefetch of the next group's entries, filter, enqueue, drain
-            auto group = [&](uint32_t m0, const uint32_t (&cur)[4], uint32_t (&nxt)[4]) {
-                // lanes past their row end load the block's first particle
-                // instead (one shared line, no extra wavefronts); hit masks them
-                float4 p[4];
+            const uint32_t m1 = m0 + 4;
+            const uint32_t* gp = ep + (m1 & 31u) * maxn + (m1 & ~31u);
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const uint32_t jk = (FW_UNCOND || m0 + k < tot) ? cur[k] : b0;
-                    p[k] = __ldg(reinterpret_cast<const float4*>(pb + (jk << 4)));
-                }
-                const uint32_t m1 = m0 + 4;
-                const uint32_t* gp = ep + (m1 & 31u) * maxn + (m1 & ~31u);
+            for (int k = 0; k < 4; ++k) nxt[k] = __ldg(gp + k * maxn);  // coalesced
 #pragma unroll
-                for (int k = 0; k < 4; ++k) nxt[k] = __ldg(gp + k * maxn);  // coalesced
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    float dx = pi.x - p[k].x, dy = pi.y - p[k].y, dz = pi.z - p[k].z;
-                    if (WRAP) {
-                        dx = min_image_rint(dx, lx, ilx);
-                        dy = min_image_rint(dy, ly, ily);
-                        dz = min_image_rint(dz, lz, ilz);
-                    }
-                    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                    const bool hit = m0 + k < tot && r2 <= rc2;
-                    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, hit);
-                    if (hit) qw[qtail + __popc(bal & lt)] = (cur[k] & 0x7FFFFFFFu) | lanebits;
-                    if (FW_PREFETCH && hit)  // phase B's vel4[j] gather then hits L1
-                        asm volatile("prefetch.global.L1 [%0];" ::"l"(vb + ((size_t)(cur[k] & 0x7FFFFFFFu) << 4)));
-                    qtail += __popc(bal);
-                }
-                // drain whole batches, then move the (< 32) leftovers to the front
-                if (qtail >= 32u) {
-                    __syncwarp();
-                    uint32_t h = 0;
-                    do {
-                        process(h, 32u);
-                        h += 32u;
-                    } while (qtail - h >= 32u);
-                    __syncwarp();
-                    const uint32_t left = qtail - h;
-                    const uint32_t mv = (uint32_t)lane < left ? qw[h + lane] : 0u;
-                    __syncwarp();
-                    if ((uint32_t)lane < left) qw[lane] = mv;
-                    __syncwarp();
-                    qtail = left;
-                }
-            };
-            uint32_t ea[4], eb[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) ea[k] = __ldg(ep + k * maxn);
-#pragma unroll 1
-            for (uint32_t m0 = 0; m0 < maxtot; m0 += 8) {
-                group(m0, ea, eb);
-                if (m0 + 4 >= maxtot) break;
-                group(m0 + 4, eb, ea);
+            for (int k = 0; k < 4; ++k) {
+                float dx, dy, dz;
+                posq_delta(a, pi, p[k], dx, dy, dz);
+                const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                const bool hit = m0 + k < tot && r2 <= rc2;
+                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, hit);
+                if (hit) qw[qtail + __popc(bal & lt)] = (cur[k] & 0x7FFFFFFFu) | lanebits;
+                if (FW_PREFETCH && hit)  // phase B's vel4[j] gather then hits L1
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(vb + ((size_t)(cur[k] & 0x7FFFFFFFu) << 4)));
+                qtail += __popc(bal);
+            }
+            // drain whole batches, then move the (< 32) leftovers to the front
+            if (qtail >= 32u) {
+                __syncwarp();
+                uint32_t h = 0;
+                do {
+                    process(h, 32u);
+                    h += 32u;
+                } while (qtail - h >= 32u);
+                __syncwarp();
+                const uint32_t left = qtail - h;
+                const uint32_t mv = (uint32_t)lane < left ? qw[h + lane] : 0u;
+                __syncwarp();
+                if ((uint32_t)lane < left) qw[lane] = mv;
+                __syncwarp();
+                qtail = left;
             }
         };
-        if (anywrap)
-            phase_a(std::integral_constant<bool, true>{});
-        else
-            phase_a(std::integral_constant<bool, false>{});
+        uint32_t ea[4], eb[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) ea[k] = __ldg(ep + k * maxn);
+#pragma unroll 1
+        for (uint32_t m0 = 0; m0 < maxtot; m0 += 8) {
+            group(m0, ea, eb);
+            if (m0 + 4 >= maxtot) break;
+            group(m0 + 4, eb, ea);
+        }
         __syncwarp();
         if (qtail > 0) process(0u, qtail);
         __syncwarp();
@@ -563,8 +573,8 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceA
                 const uint32_t i = b0 + t;
 #pragma unroll
                 for (int k = 0; k < 3; ++k) {
-                    ex[q][k] = a.ia.x[k][i];
-                    ex[q][3 + k] = a.ia.v[k][i];
+                    ex[q][k] = a.xd[k][i];  // the epilogue writes x(n+1) to the other buffer (ia.x):
+                    ex[q][3 + k] = a.ia.v[k][i];  // other blocks' close pairs still read x(n)
                 }
                 etag[q] = a.ia.tag[i];
                 esp[q] = a.ia.sp ? a.ia.sp[i] : 0u;
@@ -606,7 +616,7 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceA
             const double v[3] = {ex[qq][3], ex[qq][4], ex[qq][5]};
             double vf[3];
             integrate_particle<true, true, FUSE == FUSE_KEYS, FUSE == FUSE_STREAMS>(
-                a.ia, i, f, x, v, etag[qq], esp[qq], a.pos4n, a.vel4n, vf);
+                a.ia, i, f, x, v, etag[qq], esp[qq], nullptr, a.posqn, a.vel4n, vf);
             th[0] += vf[0];
             th[1] += vf[1];
             th[2] += vf[2];

@@ -5,6 +5,8 @@
 //   f[3]                fp32 SoA forces (accumulated in fp32)
 //   tag u32, species u8, molecule u32
 //   pos4 float4         (x - slab_centre as fp32 | tag bits)   P:234 precision model
+//                       (the builder's frozen distance frame)
+//   posq int4           (x in int32 fixed point | tag bits): the pair-force frame
 //   vel4 float4         (v as fp32 | signature bits)
 //   keys/vals u32       radix sort ping-pong; sorted keys double as cell ranks
 //   cell_start u32      [n_total_cells + 1]
@@ -103,6 +105,36 @@ __device__ __forceinline__ bool sort_key_of(const DevGrid& g, double x, double y
     return true;
 }
 
+// ------------------------------------------------- pair-force frame
+// Fixed-point position frame of the pair-force kernels (posq).  The builder's
+// fp32 slab-centre frame (pos4, frozen by inc/neighbor_table.hpp:43-44 for
+// bit-exact rows) rounds x - centre to 24 bits: 3.8e-6 at |x - c| ~ 60 (C3),
+// 7.6e-6 at ~90 (C5), which for a close pair (r ~ 1e-3) turns into a 1e-2
+// error of the pair direction.  posq keeps 32 bits per axis instead:
+//   wrap axes (single-domain periodic): q = (x - lo) * 2^32 / L taken mod
+//     2^32, so the int32 difference of two particles IS the minimum image
+//     (src/core.cpp:129-139) at L / 2^32 resolution (2.6e-8 at C3);
+//   other axes: q = (x - centre) * 2^e, the largest power of two that keeps
+//     the slab, its ghost layers and a margin inside int32.
+// The force kernels form dx = (float)(q_i - q_j) * qs: exact integer
+// difference, one rounding.
+struct PosQ {
+    double org[3];  // lo (wrap axes) or slab centre
+    double s[3];    // quanta per length unit
+    int wrap[3];
+};
+
+__device__ __forceinline__ int quant_axis(double x, double org, double s, int wrap) {
+    const long long q = __double2ll_rn(__dmul_rn(__dsub_rn(x, org), s));
+    if (wrap) return (int)(unsigned)(unsigned long long)q;  // mod 2^32
+    return (int)min(max(q, -2147483647LL), 2147483647LL);
+}
+
+__device__ __forceinline__ int4 posq_of(const PosQ& p, double x0, double x1, double x2, uint32_t tw) {
+    return make_int4(quant_axis(x0, p.org[0], p.s[0], p.wrap[0]), quant_axis(x1, p.org[1], p.s[1], p.wrap[1]),
+                     quant_axis(x2, p.org[2], p.s[2], p.wrap[2]), (int)tw);
+}
+
 // --------------------------------------------------------- integrator
 struct BoundaryArgs {
     double lo[3], hi[3], L[3];
@@ -150,7 +182,9 @@ struct IntegrateArgs {
     const uint32_t* tag;
     const uint8_t* sp;  // species (multi-species runs only, else nullptr)
     float4* pos4;
+    int4* posq;
     float4* vel4;
+    PosQ pq;
     uint32_t* keys;
     uint32_t* vals;
     DevErr* err;
@@ -189,12 +223,14 @@ __device__ __forceinline__ void block_sum4(double (&v)[4], double* out) {
 // Each half kick is its own rounding so the fp64 trajectory equals the
 // reference's phase2-then-phase1 sequence bit for bit.
 // One particle; f is the particle's force (k_integrate reads it from memory,
-// the fused pair-force kernel hands over its freshly reduced sum).
+// the fused pair-force kernel hands over its freshly reduced sum).  STREAMS
+// writes posq + vel4 (the pair kernel's inputs) and pos4 when non-null (the
+// fused epilogue skips it: only the builder reads pos4, after a permute).
 template <bool PHASE2, bool PHASE1, bool KEYS, bool STREAMS>
 __device__ __forceinline__ void integrate_particle(const IntegrateArgs& a, uint32_t i, const float f[3],
                                                    const double xin[3], const double vin[3],
                                                    uint32_t tag, uint32_t spc, float4* pos4,
-                                                   float4* vel4, double vfull[3]) {
+                                                   int4* posq, float4* vel4, double vfull[3]) {
     double xs[3], vs[3];
     bool ok = true;
     uint32_t walls = 0;  // axes whose wall reflected this particle
@@ -239,8 +275,10 @@ __device__ __forceinline__ void integrate_particle(const IntegrateArgs& a, uint3
     if (STREAMS) {
         const uint32_t sig = make_signature(tag, vs[0], vs[1], vs[2]);
         const uint32_t tw = a.sp ? (tag | (spc << 28)) : tag;  // species in bits 28+
-        pos4[i] = make_float4((float)(xs[0] - a.grid.centre[0]), (float)(xs[1] - a.grid.centre[1]),
-                              (float)(xs[2] - a.grid.centre[2]), __uint_as_float(tw));
+        if (pos4)
+            pos4[i] = make_float4((float)(xs[0] - a.grid.centre[0]), (float)(xs[1] - a.grid.centre[1]),
+                                  (float)(xs[2] - a.grid.centre[2]), __uint_as_float(tw));
+        posq[i] = posq_of(a.pq, xs[0], xs[1], xs[2], tw);
         vel4[i] = make_float4((float)vs[0], (float)vs[1], (float)vs[2], __uint_as_float(sig));
     }
 }
@@ -260,7 +298,8 @@ __global__ void __launch_bounds__(256) k_integrate(IntegrateArgs a) {
         }
         const uint32_t tag = (STREAMS || PHASE1) ? a.tag[i] : 0u;  // signature / error report
         const uint32_t spc = (STREAMS && a.sp) ? a.sp[i] : 0u;
-        integrate_particle<PHASE2, PHASE1, KEYS, STREAMS>(a, i, f, x, v, tag, spc, a.pos4, a.vel4, vf);
+        integrate_particle<PHASE2, PHASE1, KEYS, STREAMS>(a, i, f, x, v, tag, spc, a.pos4, a.posq, a.vel4,
+                                                          vf);
     }
     if (PHASE2 && a.thermo_part) {  // uniform per launch
         double s4[4] = {vf[0], vf[1], vf[2], vf[0] * vf[0] + vf[1] * vf[1] + vf[2] * vf[2]};
@@ -518,7 +557,9 @@ struct PermuteArgs {
     uint32_t* cell_start;        // [n_total_cells + 1]
     uint32_t* ostart;            // [8 n_total_cells + 1] octant starts (nullable, sub_bits >= 1)
     float4* pos4;
+    int4* posq;
     float4* vel4;
+    PosQ pq;
     double centre[3];
     uint32_t n, n_total_cells;
     int key_shift;               // 3 * sub_bits
@@ -551,6 +592,7 @@ __global__ void __launch_bounds__(256) k_permute(PermuteArgs a) {
     const uint32_t tw = a.multi ? (tag | ((uint32_t)spc << 28)) : tag;  // species in bits 28+
     a.pos4[t] = make_float4((float)(xs[0] - a.centre[0]), (float)(xs[1] - a.centre[1]),
                             (float)(xs[2] - a.centre[2]), __uint_as_float(tw));
+    a.posq[t] = posq_of(a.pq, xs[0], xs[1], xs[2], tw);
     a.vel4[t] = make_float4((float)vs[0], (float)vs[1], (float)vs[2], __uint_as_float(sig));
     // cell_start[c] = first t with rank >= c
     const uint32_t rmax = a.n_total_cells - 1u;  // clamp: a bad key already raised an error
@@ -581,8 +623,9 @@ __global__ void __launch_bounds__(256) k_streams(const double* __restrict__ x0,
                                                  const double* __restrict__ v2,
                                                  const uint32_t* __restrict__ tag,
                                                  const uint8_t* __restrict__ sp, float4* pos4,
-                                                 float4* vel4, uint32_t* sig_out, double c0,
-                                                 double c1, double c2, uint32_t n) {
+                                                 int4* posq, float4* vel4, uint32_t* sig_out,
+                                                 double c0, double c1, double c2, PosQ pq,
+                                                 uint32_t n) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double vx = v0[i], vy = v1[i], vz = v2[i];
@@ -591,6 +634,7 @@ __global__ void __launch_bounds__(256) k_streams(const double* __restrict__ x0,
     const uint32_t tw = sp ? (t | ((uint32_t)sp[i] << 28)) : t;
     pos4[i] = make_float4((float)(x0[i] - c0), (float)(x1[i] - c1), (float)(x2[i] - c2),
                           __uint_as_float(tw));
+    posq[i] = posq_of(pq, x0[i], x1[i], x2[i], tw);
     vel4[i] = make_float4((float)vx, (float)vy, (float)vz, __uint_as_float(sig));
     if (sig_out) sig_out[i] = sig;
 }
@@ -1256,23 +1300,19 @@ struct BondArgs {
     const float* ak;
     const float* at0;
     const uint32_t* index_of_tag;
-    const float4* pos4;
+    const int4* posq;   // the pair-force frame (minimum image on wrap axes by int32 wrap)
     float* f[3];
     DevErr* err;
-    float L[3], H[3];
-    int periodic[3];
+    float qs[3];        // length per posq quantum
     uint32_t n, max_tag;
     uint32_t tag_mask;  // 0x0FFFFFFF when species ride in pos4.w
 };
 
-__device__ __forceinline__ void bonded_delta(const BondArgs& a, const float4& p, const float4& q,
+__device__ __forceinline__ void bonded_delta(const BondArgs& a, const int4& p, const int4& q,
                                              float d[3]) {
-    d[0] = p.x - q.x;
-    d[1] = p.y - q.y;
-    d[2] = p.z - q.z;
-#pragma unroll
-    for (int k = 0; k < 3; ++k)
-        if (a.periodic[k]) d[k] = min_image_f(d[k], a.L[k], a.H[k]);
+    d[0] = (float)(p.x - q.x) * a.qs[0];
+    d[1] = (float)(p.y - q.y) * a.qs[1];
+    d[2] = (float)(p.z - q.z) * a.qs[2];
 }
 
 // Bonded force on particle i: every bond of i in CSR order -- harmonic
@@ -1292,8 +1332,8 @@ __device__ __forceinline__ void bonded_delta(const BondArgs& a, const float4& p,
 template <bool STYLED>
 __device__ __forceinline__ bool bond_force(const BondArgs& a, uint32_t i, float& fx, float& fy,
                                            float& fz) {
-    const float4 pi = a.pos4[i];
-    const uint32_t tag = __float_as_uint(pi.w) & a.tag_mask;
+    const int4 pi = a.posq[i];
+    const uint32_t tag = (uint32_t)pi.w & a.tag_mask;
     if (tag > a.max_tag) return false;
     const uint32_t b0 = a.boff[tag], b1 = a.boff[tag + 1];
     const uint32_t e0 = STYLED && a.aoff ? a.aoff[tag] : 0u, e1 = STYLED && a.aoff ? a.aoff[tag + 1] : 0u;
@@ -1308,7 +1348,7 @@ __device__ __forceinline__ bool bond_force(const BondArgs& a, uint32_t i, float&
             continue;
         }
         float d[3];
-        bonded_delta(a, pi, a.pos4[j], d);
+        bonded_delta(a, pi, a.posq[j], d);
         const float r = sqrtf(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
         const float k = a.bk[b], r0 = a.br0[b];
         const bool fene = STYLED && a.bstyle && a.bstyle[b] == 1;
@@ -1331,10 +1371,10 @@ __device__ __forceinline__ bool bond_force(const BondArgs& a, uint32_t i, float&
         }
         // roles: 0 -> i is end a (others: b, c); 1 -> i is the middle b (a, c);
         // 2 -> i is end c (b, a)
-        const float4 q1 = a.pos4[j1], q2 = a.pos4[j2];
-        const float4 pa = rec.z == 1 ? q1 : pi;
-        const float4 pb = rec.z == 1 ? pi : q1;
-        const float4 pc = q2;  // role 0: c; role 1: c; role 2: a (symmetric in a <-> c)
+        const int4 q1 = a.posq[j1], q2 = a.posq[j2];
+        const int4 pa = rec.z == 1 ? q1 : pi;
+        const int4 pb = rec.z == 1 ? pi : q1;
+        const int4 pc = q2;  // role 0: c; role 1: c; role 2: a (symmetric in a <-> c)
         float r1[3], r2[3];
         bonded_delta(a, pa, pb, r1);
         bonded_delta(a, pc, pb, r2);

@@ -1,11 +1,12 @@
 """Device pair/bond/body forces vs the oracle.
 
-Tolerances (north_star: "per-step forces match within 1e-5 relative in fp32"):
-  * vs the SPEC oracle (fp64 coordinates, fp64 math):
+Tolerances (north_star: "per-step forces match within 1e-5 relative in fp32"),
+both against the SPEC oracle (fp64 coordinates, fp64 math):
         ||F_gpu - F_ref||_2 / ||F_ref||_2 <= 1e-5
-  * vs the PAPER precision model (fp32 centre-relative coordinates and
-    fp32 velocities, fp64 math) -- isolates kernel arithmetic:
-        max_i |F_gpu,i - F_ref,i| / rms|F_ref| <= 1e-5
+        max_i |F_gpu,i - F_ref,i| / rms|F_ref| <= 1e-5   (every particle)
+The device pair vector comes from the int32 fixed-point frame (posq) or, for
+r < 0.05, from the fp64 state; the pair math is fp32 with the MUFU-based
+Box-Muller (|xi - xi_ref| < 4e-6) and 2^-18 fixed-point accumulation.
 """
 import numpy as np
 import pytest
@@ -17,7 +18,7 @@ import dpdsys as _sys
 pytestmark = pytest.mark.gpu
 
 REL_L2 = 1e-5
-REL_MAX_PAPER = 3e-5  # secondary, per particle vs rms; primary criterion is REL_L2
+REL_MAX = 1e-5  # per particle, relative to rms |F|
 
 
 def device_forces(box, st, step, params=None, run=None):
@@ -82,13 +83,12 @@ def test_forces_vs_oracle(L, per, step):
     p = dpd.PairParams()
     e, Fg, s = device_forces(box, st, step, p)
     Fspec = oracle_forces(e, s, obox, p, step)
-    Fpap = oracle_forces(e, s, obox, p, step, paper=True)
     rms = np.sqrt((Fspec ** 2).sum(1).mean())
     l2 = np.linalg.norm(Fg - Fspec) / np.linalg.norm(Fspec)
-    mx = np.abs(Fg - Fpap).max() / rms
-    print(f"rel L2 vs spec {l2:.2e}; max/rms vs paper model {mx:.2e}")
+    mx = np.sqrt(((Fg - Fspec) ** 2).sum(1)).max() / rms
+    print(f"rel L2 vs spec {l2:.2e}; max_i |dF_i|/rms {mx:.2e}")
     assert l2 <= REL_L2
-    assert mx <= REL_MAX_PAPER
+    assert mx <= REL_MAX
     # momentum conservation of the full-list kernel (pair symmetry of xi)
     assert np.abs(Fg.sum(0)).max() <= 1e-5 * rms * np.sqrt(len(Fg))
 
