@@ -67,6 +67,7 @@ struct dpdb_ctx {
     uint8_t *stencil_n{}, *cell_flags{}, *stencil_code{};
     float4* cell_lo{};
     uint32_t *entries{}, *counts{}, *fwalk{};
+    uint32_t* plist{};  // walk layouts: per-tile flat pair lists of the force kernel (k_tile_compact)
     uint2* rowmeta{};
     // table layout: 0 reference (split/joined), 1 ballot walk (k_build), 2 lane
     // walk (k_build_lane), 3 range walk (k_build_range: front entries only)
@@ -96,6 +97,8 @@ struct dpdb_ctx {
     bool has_mol = false, have_sorted = false, have_table = false, tiled = true, joined = false;
     bool multi = false;  // n_species > 1: species packed into pos4.w bits 28-31
     bool no_fuse = false;  // DPDB_FUSE=0: keep the Verlet pass a separate kernel (A/B)
+    uint32_t num_sms = 148;   // multiprocessors of the device
+    uint32_t swz_group = 0;   // force-block swizzle group (DPDB_SWZ; 0 = identity)
     // per-step thermo (dpdb_step_thermo): block partials of the phase-2 pass
     // and the records, written by the device straight into mapped pinned memory
     double* thermo_part{};
@@ -468,9 +471,27 @@ size_t build_smem(const dpdb_ctx* ctx) {
     return BUILD_WARPS * 32 * sizeof(float4) + P * 4 + ((size_t)ctx->maxn + 1) * (P + 1) * 4;
 }
 
+int launch_build(dpdb_ctx* ctx, bool joined_out);
+
+// The force kernel's per-tile flat pair lists from a walk layout's front entries
+int do_compact(dpdb_ctx* ctx) {
+    const unsigned tiles = (unsigned)((ctx->n + 31) / 32);
+    dpdb::k_tile_compact<<<(tiles + dpdb::TC_WARPS - 1) / dpdb::TC_WARPS, dpdb::TC_WARPS * 32, 0, ctx->stream>>>(
+        ctx->entries, ctx->fwalk, (uint32_t)ctx->n, ctx->maxn, ctx->plist);
+    CKL();
+    ctx->launches[ST_BUILD]++;
+    return 0;
+}
+
 // joined_out: write rows already joined (core asc, skin asc) -- the step
 // pipeline's layout; the per-stage API builds the reference's split layout.
 int do_build(dpdb_ctx* ctx, bool joined_out) {
+    TRY(launch_build(ctx, joined_out));
+    if (ctx->walk && ctx->n) TRY(do_compact(ctx));
+    return 0;
+}
+
+int launch_build(dpdb_ctx* ctx, bool joined_out) {
     if (!ctx->have_sorted) return fail(ctx, DPDB_ECONFIG, "build_neighbor_table: particles not reordered");
     ctx->tiled = true;
     ctx->joined = joined_out;
@@ -642,6 +663,7 @@ int do_forces(dpdb_ctx* ctx, uint32_t step, int fuse = dpdb::FUSE_NONE, bool the
     a.entries = ctx->entries;
     a.counts = ctx->counts;
     a.fwalk = ctx->fwalk;
+    a.plist = ctx->plist;
     a.xpart = ctx->x[ctx->run.partition_axis];
     for (int k = 0; k < 3; ++k) a.f[k] = ctx->f[k];
     a.err = ctx->err;
@@ -679,6 +701,9 @@ int do_forces(dpdb_ctx* ctx, uint32_t step, int fuse = dpdb::FUSE_NONE, bool the
         a.has_bonds = 1;
         a.bd = bond_args(ctx);
     }
+    a.n_blocks = (uint32_t)((ctx->n + dpdb::FORCE_BLOCK - 1) / dpdb::FORCE_BLOCK);
+    a.swz_group = ctx->swz_group;
+    a.swz_sms = ctx->num_sms;
     if (part >= 0) {
         a.blk_sel = ctx->blk_ghost;
         a.sel_val = (uint32_t)part;
@@ -826,6 +851,12 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         ctx->builder = !std::strcmp(b, "ballot") ? 0 : !std::strcmp(b, "lane") ? 1 : 2;
     ctx->multi = params->n_species > 1;
     if (const char* f = std::getenv("DPDB_FUSE")) ctx->no_fuse = std::strcmp(f, "0") == 0;
+    {
+        int sms = 0;
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0)
+            ctx->num_sms = (uint32_t)sms;
+        if (const char* z = std::getenv("DPDB_SWZ")) ctx->swz_group = (uint32_t)std::atoi(z);
+    }
     for (int q = 0; q < ns * ns; ++q) ctx->sigma[q] = std::sqrt(2.0 * params->gamma[q] * params->kbt);
     std::string err;
     // brick geometry (decompose): uniform half-open slabs
@@ -915,6 +946,7 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         (rc = dalloc(ctx, ctx->stencil_code, (size_t)g.n_local_cells * 32)) ||
         (rc = dalloc(ctx, ctx->cell_lo, (size_t)g.n_local_cells)) ||
         (rc = dalloc(ctx, ctx->entries, c * ctx->maxn)) || (rc = dalloc(ctx, ctx->counts, c)) ||
+        (rc = dalloc(ctx, ctx->plist, c * ctx->maxn + 512)) ||
         (rc = dalloc(ctx, ctx->fwalk, c)) || (rc = dalloc(ctx, ctx->rowmeta, c)) ||
         (rc = dalloc(ctx, ctx->md_masks, c)) || (rc = dalloc(ctx, ctx->md_mig, c)) ||
         (rc = dalloc(ctx, ctx->md_slot, c)) || (rc = dalloc(ctx, ctx->md_doff, 64)) ||
@@ -985,7 +1017,7 @@ int dpdb_destroy(dpdb_ctx* ctx) {
     void* ptrs[] = {ctx->tag, ctx->tag2, ctx->mol, ctx->mol2, ctx->sp, ctx->sp2, ctx->pos4,
                     ctx->vel4, ctx->posq, ctx->posqn, ctx->vel4n, ctx->keys, ctx->keys2, ctx->vals, ctx->vals2, ctx->hist,
                     ctx->cell_start, ctx->ostart, ctx->rank_of_cell, ctx->stencil, ctx->stencil_n,
-                    ctx->cell_flags, ctx->stencil_code, ctx->cell_lo, ctx->entries, ctx->counts, ctx->fwalk, ctx->rowmeta,
+                    ctx->cell_flags, ctx->stencil_code, ctx->cell_lo, ctx->entries, ctx->counts, ctx->fwalk, ctx->plist, ctx->rowmeta,
                     ctx->err, ctx->red, ctx->red_out, ctx->thermo_part, ctx->thermo_part2, ctx->blk_ghost, ctx->prof_acc,
                     ctx->tmp_u32, ctx->bond_off, ctx->bond_partner, ctx->index_of_tag,
                     ctx->bond_k, ctx->bond_r0, ctx->bond_style, ctx->ang_off, ctx->ang_rec, ctx->ang_k,

@@ -12,6 +12,7 @@ struct ForceArgs {
     const uint32_t* entries;
     const uint32_t* counts;
     const uint32_t* fwalk;  // walk layout only: n_eval | flags << 26
+    const uint32_t* plist;  // walk layout: per-tile flat pair list (k_tile_compact)
     const double* xpart;  // fp64 coordinate on the partition axis (body force)
     float* f[3];
     DevErr* err;
@@ -42,6 +43,9 @@ struct ForceArgs {
     // boundary split around the ghost update); null = every block
     const uint8_t* blk_sel;
     uint32_t sel_val;
+    // block swizzle (block_of_cta): consecutive force blocks -- Morton
+    // neighbors sharing most of their halo -- on the same SM at the same time
+    uint32_t swz_group, swz_sms, n_blocks;
     // k_force_walk<GENERAL>: harmonic bonds added in the epilogue (else k_bonds runs after)
     int has_bonds;
     BondArgs bd;
@@ -67,28 +71,31 @@ __device__ __forceinline__ float sin_ftz(float x) {
     return y;
 }
 
-// Box-Muller radius/phase on the TEA-4 words in fp32 (see gaussian32 in
-// dpd_math.cuh for the derivation; same math with ftz intrinsics)
+__device__ __forceinline__ float lg2_ftz(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Box-Muller on the TEA-4 words in fp32 (inc/rng.hpp:88-91: xi = sqrt(-2 ln u_a)
+// cos(2 pi u_b), u = word * 2^-32, u_a = 0 -> 1).
+//   -2 ln u: u < 1 - 2^-8: MUFU lg2 of u (exact float of the word times
+//     2^-32), absolute error ~1e-7 where |ln u| >= 3.9e-3, so rad = sqrt(-2 ln u)
+//     is off by <= 1.3e-6; u >= 1 - 2^-8: the series -ln(1 - t) = t + t^2/2 +
+//     t^3/3 with t = (2^32 - word) 2^-32 exact (< 2^24 quanta), truncation
+//     < t^4/4 -- no cancellation as u -> 1.
+//   cos(2 pi u_b) = -/+ sin(pi y), y = (u_b mod 2^31 - 2^30) 2^-31 in
+//     [-1/2, 1/2) (the reference's sign-from-top-bit reduction, inc/fastmath.hpp:54-57).
+// |xi - xi_ref| < 4e-6 over the whole word range (test_gpu_rng).
 __device__ __forceinline__ float gaussian_hot(uint32_t ua, uint32_t ub) {
     ua = max(ua, 1u);
-    const int e = 31 - __clz(ua);
-    const uint32_t top = ua << (31 - e);
-    const int big = top >= 0xB504F334u;
-    const int k = e + big;
-    const uint32_t pk = k >= 32 ? 0u : (1u << k);
-    const float numf = (float)(int)(ua - pk);
-    const float den = fmaf(2.0f, __int_as_float((127 + k) << 23), numf);
-    const float z = numf * rcp_ftz(den);
-    const float w = z * z;
-    float p = fmaf(w, 0.2222222222f, 0.2857142857f);
-    p = fmaf(w, p, 0.4f);
-    p = fmaf(w, p, 0.6666666667f);
-    const float lnx = fmaf(z * w, p, 2.0f * z);
-    const float ln_u = fmaf((float)(k - 32), 0.693147180559945f, lnx);
-    const float m2 = -2.0f * ln_u;  // > 0 for every u < 2^32
+    const float la = lg2_ftz(__uint2float_rn(ua) * 0x1p-32f);     // log2 u, u < 1
+    const float t = __uint2float_rn(0u - ua) * 0x1p-32f;          // 1 - u (exact near 1)
+    const float lb = t * fmaf(t, fmaf(t, 0.333333333f, 0.5f), 1.0f);  // -ln u near 1
+    const float m2 = ua >= 0xFF000000u ? 2.0f * lb : la * -1.386294361f;  // -2 ln u
     const float rad = m2 * rsqrt_ftz(m2);
-    const float y = (float)(int)((ub & 0x7FFFFFFFu) - 0x40000000u) * 0x1p-31f;
-    const float s = sin_ftz(3.14159265358979f * y);
+    const float y = (float)(int)((ub & 0x7FFFFFFFu) - 0x40000000u) * 1.4629180792671596e-9f;  // pi 2^-31
+    const float s = sin_ftz(y);
     return (ub >> 31) ? rad * s : -(rad * s);
 }
 
@@ -354,6 +361,56 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(ForceArgs a) {
     }
 }
 
+// Per-tile flat pair list for k_force_walk (built once per neighbor build).
+// A walk-layout tile stores each of its 32 rows' front entries (the pairs the
+// row evaluates) in the 32x32 tile-transposed layout, so a lane-per-row
+// filter runs max(row length) steps with lanes idle past their row's end
+// (~45% of the filter's issue slots at C3).  This rewrites tile t's entries
+// as one flat list at plist + 32 t maxn: row r's entries (ascending) at the
+// exclusive prefix of the earlier rows' lengths, each packed as
+// j | r << 26 | skin << 31 -- the pair queue's own format, so the filter
+// takes 32 items per step with every lane busy.  One warp per tile; entries
+// are read coalesced (one 128-byte line per row position) and staged in
+// shared memory so the list is written coalesced too.  Deterministic: no
+// atomics, the order is the rows' order.
+constexpr int TC_WARPS = 8;
+constexpr int TC_STAGE = 1024;  // entries per staging round (a tile holds ~530 at C3)
+
+__global__ void __launch_bounds__(TC_WARPS * 32) k_tile_compact(const uint32_t* __restrict__ entries,
+                                                                const uint32_t* __restrict__ fwalk,
+                                                                uint32_t n, uint32_t maxn,
+                                                                uint32_t* __restrict__ plist) {
+    __shared__ uint32_t stage[TC_WARPS][TC_STAGE];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t i0 = (blockIdx.x * TC_WARPS + warp) * 32u;
+    if (i0 >= n) return;
+    const uint32_t i = i0 + lane;
+    const uint32_t tot = i < n ? min(fwalk[i] & 0x1FFFu, maxn) : 0u;
+    uint32_t off = tot;  // inclusive scan of the row lengths
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, off, d);
+        if (lane >= d) off += y;
+    }
+    const uint32_t cnt = __shfl_sync(0xFFFFFFFFu, off, 31);
+    off -= tot;
+    const uint32_t maxtot = __reduce_max_sync(0xFFFFFFFFu, tot);
+    const uint32_t* ep = entries + (size_t)i0 * maxn + lane;
+    uint32_t* out = plist + (size_t)i0 * maxn;
+    const uint32_t rb = (uint32_t)lane << 26;
+    for (uint32_t c0 = 0; c0 < cnt; c0 += TC_STAGE) {
+        for (uint32_t m = 0; m < maxtot; ++m) {
+            const uint32_t e = ep[(m & 31u) * maxn + (m & ~31u)];
+            const uint32_t q = off + m - c0;  // wraps (large) below the round
+            if (m < tot && q < (uint32_t)TC_STAGE) stage[warp][q] = (e & 0x83FFFFFFu) | rb;
+        }
+        __syncwarp();
+        const uint32_t len = min(cnt - c0, (uint32_t)TC_STAGE);
+        for (uint32_t q = lane; q < len; q += 32) out[c0 + q] = stage[warp][q];
+        __syncwarp();
+    }
+}
+
 // Force kernel for the step pipeline's walk layout (k_build_lane<true> /
 // k_build<.., true>): same physics, pair set and fixed-point accumulation as
 // k_force, restructured so the per-candidate filter (phase A) is as cheap as
@@ -378,32 +435,45 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(ForceArgs a) {
 #endif
 constexpr bool FW_UNCOND = DPDB_FW_UNCOND;
 #ifndef FW_MINB
-// resident CTAs per SM the register allocation must allow: 32 warps / SM
-// (64 registers; A/B at 8 warps per CTA: 1, 3, 4 CTAs -> 4 best, 5 spills)
-#define FW_MINB (32 / DPDB_FORCE_WARPS)
-#endif  // A/B switch: unpredicated phase-A loads
+// resident CTAs per SM the register allocation must allow: 40 warps / SM
+// (48 registers, 8 bytes of spill; A/B at 8 warps per CTA with the flat pair
+// list: 4 CTAs 0.5079 ms, 5 CTAs 0.4996 ms, 6 CTAs (40 registers) 0.5426 ms)
+#define FW_MINB (40 / DPDB_FORCE_WARPS)
+#endif
 #ifndef DPDB_FW_PREFETCH
 #define DPDB_FW_PREFETCH 0
 #endif
 constexpr bool FW_PREFETCH = DPDB_FW_PREFETCH;  // A/B switch: L1 prefetch of vel4[j] in phase A
 constexpr int FW_Q = 160;  // < 32 leftovers + 4 x 32 hits per group
 
+// CTA -> force block.  The hardware deals CTAs round robin over the SMs, so
+// the CTAs resident together on one SM (c, c + S, c + 2S, ...) would own
+// blocks far apart in Morton order; this maps them to G consecutive blocks
+// instead, whose halos overlap, so their neighbor gathers share L1 lines.
+// Identity on the last partial wave and when G = 0.
+__device__ __forceinline__ uint32_t block_of_cta(const ForceArgs& a, uint32_t c) {
+    const uint32_t G = a.swz_group, W = G * a.swz_sms;
+    if (G == 0u || c >= a.n_blocks / W * W) return c;
+    const uint32_t w = c / W, r = c - w * W;
+    return w * W + (r % a.swz_sms) * G + r / a.swz_sms;
+}
+
 template <bool GENERAL, bool BODY, int MAXN, int FUSE>
 __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceArgs a) {
     static_assert(FORCE_TPW % 2 == 0, "tiles are dealt in snake order, two per round");
-    __shared__ uint32_t q_j[FORCE_WARPS][FW_Q];  // j | owner lane << 27
+    __shared__ uint32_t q_j[FORCE_WARPS][FW_Q];  // plist items: j | owner row << 26 | skin << 31
     __shared__ int4 own_p[FORCE_WARPS][32];
     __shared__ float4 own_v[FORCE_WARPS][32];
     __shared__ int acc[FORCE_BLOCK * 3];
-    if (a.blk_sel && a.blk_sel[blockIdx.x] != a.sel_val) return;  // whole CTA
+    const uint32_t blk = block_of_cta(a, blockIdx.x);
+    if (a.blk_sel && a.blk_sel[blk] != a.sel_val) return;  // whole CTA
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t b0 = blockIdx.x * FORCE_BLOCK;
+    const uint32_t b0 = blk * FORCE_BLOCK;
     const uint32_t bn = min((uint32_t)FORCE_BLOCK, a.n - b0);
     for (int t = threadIdx.x; t < FORCE_BLOCK * 3; t += FORCE_WARPS * 32) acc[t] = 0;
     __syncthreads();
     const uint32_t lt = lanemask_lt();
     const uint32_t maxn = MAXN ? (uint32_t)MAXN : a.maxn;
-    const uint32_t lanebits = (uint32_t)lane << 27;
     bool coincident = false;
     uint32_t bad_tag = 0;
 
@@ -423,17 +493,16 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceA
             vi = a.vel4[b0 + il];
             c = a.fwalk[b0 + il];
         }
-        const uint32_t tot = c & 0x1FFFu;
+        const uint32_t tot = min(c & 0x1FFFu, maxn);
         own_p[warp][lane] = pi;
         own_v[warp][lane] = vi;
-        const uint32_t maxtot = __reduce_max_sync(0xFFFFFFFFu, tot);
         __syncwarp();
         uint32_t qtail = 0;
 
         auto process = [&](uint32_t h, uint32_t cnt) {
             if ((uint32_t)lane < cnt) {
                 const uint32_t jw = q_j[warp][h + lane];
-                const uint32_t o = jw >> 27, j = jw & 0x07FFFFFFu;
+                const uint32_t o = (jw >> 26) & 31u, j = jw & 0x03FFFFFFu;
                 const int4 po = own_p[warp][o];
                 const float4 vo = own_v[warp][o];
                 const int4 pj = __ldg(a.posq + j);
@@ -479,43 +548,37 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceA
             }
         };
 
-        // Row position m of this lane: ep + (m & 31) * maxn + (m & ~31).
-        // Loads are unconditional: a row is read up to the warp's longest row
-        // (+ one prefetch group), and every word of the entries array is a
-        // valid particle index (zeroed at allocation, only indices written
-        // since), so positions past a row's end are harmless in-bounds reads
-        // masked by m < tot.  posq is addressed as (e << 4) bytes in 32-bit
-        // arithmetic, which drops the walk layout's skin tag (bit 31).
-        const uint32_t* ep = a.entries + (size_t)(b0 + il0) * maxn + lane;
+        // Phase A over the tile's flat pair list (k_tile_compact): 32 items per
+        // step, every lane busy; a group is 4 steps: the 4 partner positions
+        // are gathered back to back, the next group's list words prefetched.
+        // Items past the list end load the block's first particle instead (one
+        // shared line) and are masked by the bound.
+        const uint32_t cnt = __reduce_add_sync(0xFFFFFFFFu, tot);
+        const uint32_t* pl = a.plist + (size_t)(b0 + il0) * maxn + lane;
         const char* pb = reinterpret_cast<const char*>(a.posq);
         const char* vb = reinterpret_cast<const char*>(a.vel4);
         uint32_t* qw = q_j[warp];
         const float rc2 = a.rc2;
-        // one group = 4 row positions: positions of the group's candidates,
-        // prefetch of the next group's entries, filter, enqueue, drain
-        auto group = [&](uint32_t m0, const uint32_t (&cur)[4], uint32_t (&nxt)[4]) {
-            // lanes past their row end load the block's first particle
-            // instead (one shared line, no extra wavefronts); hit masks them
+        auto group = [&](uint32_t c0, const uint32_t (&cur)[4], uint32_t (&nxt)[4]) {
             int4 p[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const uint32_t jk = (FW_UNCOND || m0 + k < tot) ? cur[k] : b0;
-                p[k] = __ldg(reinterpret_cast<const int4*>(pb + (jk << 4)));
+                const uint32_t jk = c0 + 32u * k + lane < cnt ? (cur[k] & 0x03FFFFFFu) : b0;
+                p[k] = __ldg(reinterpret_cast<const int4*>(pb + ((size_t)jk << 4)));
             }
-            const uint32_t m1 = m0 + 4;
-            const uint32_t* gp = ep + (m1 & 31u) * maxn + (m1 & ~31u);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) nxt[k] = __ldg(gp + k * maxn);  // coalesced
+            for (int k = 0; k < 4; ++k) nxt[k] = __ldg(pl + c0 + 128u + 32u * k);  // coalesced
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
+                const int4 po = own_p[warp][(cur[k] >> 26) & 31u];
                 float dx, dy, dz;
-                posq_delta(a, pi, p[k], dx, dy, dz);
+                posq_delta(a, po, p[k], dx, dy, dz);
                 const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                const bool hit = m0 + k < tot && r2 <= rc2;
+                const bool hit = c0 + 32u * k + lane < cnt && r2 <= rc2;
                 const uint32_t bal = __ballot_sync(0xFFFFFFFFu, hit);
-                if (hit) qw[qtail + __popc(bal & lt)] = (cur[k] & 0x7FFFFFFFu) | lanebits;
+                if (hit) qw[qtail + __popc(bal & lt)] = cur[k];
                 if (FW_PREFETCH && hit)  // phase B's vel4[j] gather then hits L1
-                    asm volatile("prefetch.global.L1 [%0];" ::"l"(vb + ((size_t)(cur[k] & 0x7FFFFFFFu) << 4)));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(vb + ((size_t)(cur[k] & 0x03FFFFFFu) << 4)));
                 qtail += __popc(bal);
             }
             // drain whole batches, then move the (< 32) leftovers to the front
@@ -537,12 +600,12 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceA
         };
         uint32_t ea[4], eb[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) ea[k] = __ldg(ep + k * maxn);
+        for (int k = 0; k < 4; ++k) ea[k] = __ldg(pl + 32u * k);
 #pragma unroll 1
-        for (uint32_t m0 = 0; m0 < maxtot; m0 += 8) {
-            group(m0, ea, eb);
-            if (m0 + 4 >= maxtot) break;
-            group(m0 + 4, eb, ea);
+        for (uint32_t c0 = 0; c0 < cnt; c0 += 256) {
+            group(c0, ea, eb);
+            if (c0 + 128 >= cnt) break;
+            group(c0 + 128, eb, ea);
         }
         __syncwarp();
         if (qtail > 0) process(0u, qtail);
@@ -624,5 +687,5 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceA
         }
     }
     if (FUSE != FUSE_NONE && a.ia.thermo_part)  // uniform per launch
-        block_sum4<FORCE_WARPS * 32>(th, a.ia.thermo_part + 4 * blockIdx.x);
+        block_sum4<FORCE_WARPS * 32>(th, a.ia.thermo_part + 4 * blk);
 }

@@ -105,25 +105,29 @@ def test_steady_double_poiseuille_viscosity():
     sigma = 4.5, rho = 6, kT = 0.5, dt = 0.001, g = 0.055, a = 0 in a 12 x 32 x 8
     box (the paper's 12 x 8 x 8 channel, 4x wider along the neutral y axis for
     4x the samples; drive x, profile and partition along z); the parabolic fit
-    of the folded profile gives the viscosity, paper 2.089 +- 0.009
-    (acceptance window [2.02, 2.16], SPEC invariants; seeds 7-10 measured
-    2.075, 2.091, 2.089, 2.042)."""
-    L = (12.0, 32.0, 8.0)
-    box, obox, st = _sys.fluid(L, 6.0, seed=7, kbt=0.5)
-    gamma = 4.5 ** 2 / (2 * 0.5)
-    p = dpd.PairParams.make(1, 0.0, gamma, 0.5, 1.0, 1.0, 0.001)
-    run = dpd.RunConfig(body_force=0.055, drive_axis=0, partition_axis=2)
-    e = _sys.engine(box, st, params=p, run=run)
-    e.setup()
-    e.step(60000)  # ~1.3 viscous times d^2 / nu to steady state
-    e.profile_reset(32, 2, 0)
-    for _ in range(600):
-        e.step(100)
-        e.profile_sample()
-    sv, cnt, ns = e.profile()
-    prof = velocity_profile(sv, cnt, ns, 0.0, 8.0, fold=True)
-    mu, se, rel = estimate_viscosity(prof.centers - 4.0, -prof.mean_v, 0.055, 6.0, 4.0)
-    assert 2.02 <= mu <= 2.16, (mu, se, rel)
+    of the folded profile gives the viscosity, paper 2.089 +- 0.009.  The
+    estimate of one run scatters by ~0.02 (seeds 7-14: 2.009-2.090, mean
+    2.062), so the acceptance window [2.02, 2.16] is applied to the mean of
+    three independent runs."""
+    mus = []
+    for seed in (7, 8, 9):
+        L = (12.0, 32.0, 8.0)
+        box, obox, st = _sys.fluid(L, 6.0, seed=seed, kbt=0.5)
+        gamma = 4.5 ** 2 / (2 * 0.5)
+        p = dpd.PairParams.make(1, 0.0, gamma, 0.5, 1.0, 1.0, 0.001)
+        run = dpd.RunConfig(body_force=0.055, drive_axis=0, partition_axis=2)
+        e = _sys.engine(box, st, params=p, run=run)
+        e.setup()
+        e.step(60000)  # ~1.3 viscous times d^2 / nu to steady state
+        e.profile_reset(32, 2, 0)
+        for _ in range(600):
+            e.step(100)
+            e.profile_sample()
+        sv, cnt, ns = e.profile()
+        prof = velocity_profile(sv, cnt, ns, 0.0, 8.0, fold=True)
+        mu, se, rel = estimate_viscosity(prof.centers - 4.0, -prof.mean_v, 0.055, 6.0, 4.0)
+        mus.append(mu)
+    assert 2.02 <= float(np.mean(mus)) <= 2.16, mus
 
 
 def poiseuille_engine(L, rho, a, sigma, kbt, dt, g, seed):
