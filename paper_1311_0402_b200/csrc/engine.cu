@@ -487,7 +487,9 @@ int do_compact(dpdb_ctx* ctx) {
 // pipeline's layout; the per-stage API builds the reference's split layout.
 int do_build(dpdb_ctx* ctx, bool joined_out) {
     TRY(launch_build(ctx, joined_out));
-    if (ctx->walk && ctx->n) TRY(do_compact(ctx));
+    // the range builder appends the flat lists itself; the lane / ballot walk
+    // layouts are compacted from their tile-transposed rows
+    if (ctx->walk && ctx->walk != 3 && ctx->n) TRY(do_compact(ctx));
     return 0;
 }
 
@@ -510,6 +512,7 @@ int launch_build(dpdb_ctx* ctx, bool joined_out) {
     a.counts = ctx->counts;
     a.fwalk = ctx->fwalk;
     a.rowmeta = ctx->rowmeta;
+    a.plist = ctx->plist;
     a.force_block = dpdb::FORCE_BLOCK;
     a.err = ctx->err;
     a.n_local = (uint32_t)ctx->n;
@@ -1457,6 +1460,53 @@ namespace {
 //    skin[0,s1) skin[s2,ns) core[c1,c2) skin[s1,s2);
 //  2 (k_build_lane): n_front = fwalk & 0x1FFF entries ascending from the front,
 //    the rest reversed from the back; bit 31 marks skin entries.
+// Front entries (j | skin << 31, ascending) of every row from the range
+// builder's per-tile flat lists: tile t's list holds sum_r fwalk[32t + r]
+// items j | r << 26 | skin << 31, each row's items in ascending order.
+int walk3_front(dpdb_ctx* ctx, const std::vector<uint32_t>& fw, std::vector<std::vector<uint32_t>>& front) {
+    const size_t n = ctx->n, maxn = ctx->maxn;
+    std::vector<uint32_t> pl(((n + 31) & ~size_t(31)) * maxn);
+    CK(cudaMemcpy(pl.data(), ctx->plist, pl.size() * 4, cudaMemcpyDeviceToHost));
+    front.assign(n, {});
+    for (size_t t0 = 0; t0 < n; t0 += 32) {
+        size_t cnt = 0;
+        for (size_t i = t0; i < std::min(n, t0 + 32); ++i) cnt += std::min<size_t>(fw[i] & 0x1FFFu, maxn);
+        for (size_t k = 0; k < cnt; ++k) {
+            const uint32_t e = pl[t0 * maxn + k];
+            const size_t i = t0 + ((e >> 26) & 31u);
+            if (i < n) front[i].push_back((e & 0x03FFFFFFu) | (e & 0x80000000u));
+        }
+    }
+    return 0;
+}
+
+// Full-row counts (core | skin << 13 | flags << 26, as k_build_range writes
+// for the reference layout) of a layout-3 table: front entries + their
+// in-block transposes.
+int walk3_counts(dpdb_ctx* ctx, std::vector<uint32_t>& fw, std::vector<std::vector<uint32_t>>& front,
+                 std::vector<std::vector<uint32_t>>& extra, std::vector<uint32_t>& cnt) {
+    const size_t n = ctx->n;
+    fw.resize(n);
+    cnt.resize(n);
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(fw.data(), ctx->fwalk, n * 4, cudaMemcpyDeviceToHost));
+    TRY(walk3_front(ctx, fw, front));
+    extra.assign(n, {});
+    for (size_t i = 0; i < n; ++i)
+        for (uint32_t e : front[i]) {
+            const size_t j = e & 0x7FFFFFFFu;
+            if (j > i && j < n && j / dpdb::FORCE_BLOCK == i / dpdb::FORCE_BLOCK)
+                extra[j].push_back((uint32_t)i | (e & 0x80000000u));
+        }
+    for (size_t i = 0; i < n; ++i) {
+        uint32_t nc = 0, ns = 0;
+        for (uint32_t e : front[i]) (e >> 31 ? ns : nc)++;
+        for (uint32_t e : extra[i]) (e >> 31 ? ns : nc)++;
+        cnt[i] = std::min(nc, 8191u) | (std::min(ns, 8191u) << 13) | (fw[i] & 0xFC000000u);
+    }
+    return 0;
+}
+
 int unwalk(dpdb_ctx* ctx) {
     if (!ctx->walk) return 0;
     const int layout = ctx->walk;
@@ -1466,23 +1516,20 @@ int unwalk(dpdb_ctx* ctx) {
     std::vector<uint32_t> raw(rows * maxn), cnt(n), fw(n), out(rows * maxn, 0u);
     std::vector<uint2> meta(n);
     CK(cudaStreamSynchronize(ctx->stream));
-    CK(cudaMemcpy(raw.data(), ctx->entries, raw.size() * 4, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(cnt.data(), ctx->counts, n * 4, cudaMemcpyDeviceToHost));
+    if (layout != 3) {
+        CK(cudaMemcpy(raw.data(), ctx->entries, raw.size() * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(cnt.data(), ctx->counts, n * 4, cudaMemcpyDeviceToHost));
+    }
     if (layout == 1) CK(cudaMemcpy(meta.data(), ctx->rowmeta, n * sizeof(uint2), cudaMemcpyDeviceToHost));
     if (layout >= 2) CK(cudaMemcpy(fw.data(), ctx->fwalk, n * 4, cudaMemcpyDeviceToHost));
-    // layout 3 keeps only the front entries: the in-block j < i entries of row
-    // i are the transposes of front entries (j -> i, j > i, same force block)
-    std::vector<std::vector<uint32_t>> extra(layout == 3 ? n : 0);
-    if (layout == 3)
-        for (size_t i = 0; i < n; ++i) {
-            const uint32_t nf = std::min<uint32_t>(fw[i] & 0x1FFFu, (uint32_t)maxn);
-            for (uint32_t k = 0; k < nf; ++k) {
-                const uint32_t e = raw[((i & ~size_t(31)) + (k & 31)) * maxn + (k & ~size_t(31)) + (i & 31)];
-                const size_t j = e & 0x7FFFFFFFu;
-                if (j > i && j < n && j / dpdb::FORCE_BLOCK == i / dpdb::FORCE_BLOCK)
-                    extra[j].push_back((uint32_t)i | (e & 0x80000000u));
-            }
-        }
+    // layout 3: the front entries live in the tiles' flat lists (k_build_range);
+    // the in-block j < i entries of row i are the transposes of front entries
+    // (j -> i, j > i, same force block); the full rows' counts follow
+    std::vector<std::vector<uint32_t>> front(layout == 3 ? n : 0), extra(layout == 3 ? n : 0);
+    if (layout == 3) {
+        TRY(walk3_counts(ctx, fw, front, extra, cnt));
+        CK(cudaMemcpy(ctx->counts, cnt.data(), n * 4, cudaMemcpyHostToDevice));
+    }
     auto idx = [&](size_t i, size_t k) { return ((i & ~size_t(31)) + (k & 31)) * maxn + (k & ~size_t(31)) + (i & 31); };
     std::vector<uint32_t> row(maxn), core, skin;
     for (size_t i = 0; i < n; ++i) {
@@ -1504,7 +1551,10 @@ int unwalk(dpdb_ctx* ctx) {
             core.clear();
             skin.clear();
             auto put = [&](uint32_t e) { (e >> 31 ? skin : core).push_back(e & 0x7FFFFFFFu); };
-            for (uint32_t k = 0; k < nf; ++k) put(raw[idx(i, k)]);
+            if (layout == 3)
+                for (uint32_t e : front[i]) put(e);
+            else
+                for (uint32_t k = 0; k < nf; ++k) put(raw[idx(i, k)]);
             if (layout == 2)
                 for (uint32_t q = 0; q < nb; ++q) put(raw[idx(i, maxn - 1 - q)]);
             else
@@ -1747,7 +1797,13 @@ int dpdb_table_stats(dpdb_ctx* ctx, double* mean_row, double* mean_core, uint32_
     TRY(require_ctx(ctx));
     if (!ctx->have_table) return fail(ctx, DPDB_ECONFIG, "table_stats: no table");
     std::vector<uint32_t> cnt(ctx->n);
-    CK(cudaMemcpy(cnt.data(), ctx->counts, ctx->n * 4, cudaMemcpyDeviceToHost));
+    if (ctx->walk == 3) {  // the range builder's walk layout carries no full-row counts
+        std::vector<uint32_t> fw;
+        std::vector<std::vector<uint32_t>> front, extra;
+        TRY(walk3_counts(ctx, fw, front, extra, cnt));
+    } else {
+        CK(cudaMemcpy(cnt.data(), ctx->counts, ctx->n * 4, cudaMemcpyDeviceToHost));
+    }
     double s = 0, sc = 0;
     uint32_t mx = 0;
     for (uint32_t c : cnt) {
@@ -1826,7 +1882,7 @@ int dpdb_rdf(dpdb_ctx* ctx, uint32_t nbins, double rmax, uint64_t* hist) {
     if (nbins < 1 || nbins > 8192) return fail(ctx, DPDB_ECONFIG, "rdf: 1..8192 bins");
     if (!(rmax > 0) || rmax > ctx->params.r_c + ctx->run.skin + 1e-12)
         return fail(ctx, DPDB_ECONFIG, "rdf: 0 < rmax <= r_c + skin (the table's reach)");
-    if (ctx->walk == 1 || ctx->walk == 2) TRY(unwalk(ctx));  // lane/ballot walk orders: back to reference rows
+    TRY(unwalk(ctx));  // walk layouts: back to reference rows
     TRY(do_streams(ctx, nullptr));  // pos4 of the current state (the fused loop writes posq only)
     unsigned long long* d = reinterpret_cast<unsigned long long*>(ctx->tmp_u32);
     if ((size_t)nbins * 2 > ctx->n_pad) return fail(ctx, DPDB_ECONFIG, "rdf: more bins than scratch");

@@ -652,6 +652,7 @@ struct BuildArgs {
     uint32_t* counts;
     uint32_t* fwalk;    // walk layout: n_eval | force-wrap-flags << 26
     uint2* rowmeta;     // walk layout: (c1 | c2 << 16, s1 | s2 << 16)
+    uint32_t* plist;    // k_build_range walk layout: per-tile flat pair lists (j | r << 26 | skin << 31)
     DevErr* err;
     uint32_t n_local, maxn, n_local_cells;
     uint32_t force_block;  // power of two
@@ -995,11 +996,17 @@ __global__ void __launch_bounds__(256) k_build_lane(BuildArgs a) {
 // GH: the context has ghost rows (a brick); only then is each hit tested for a
 //     ghost partner (the block's blk_ghost flag).
 //  WALK: only the entries the force kernel evaluates (j outside the block or
-//        j > i), ascending, skin tagged with bit 31; fwalk = n_front | flags.
-//        The in-block j < i entries are not stored -- they are exactly the
-//        transposes of the block's front entries (unwalk restores them) --
-//        but they are counted (shared-memory integer adds, order-free) so
-//        counts and the overflow check equal the reference's full rows.
+//        j > i) -- the row's "front" entries -- go to the tile's flat pair
+//        list (the force kernel's input): at each walk step the lanes with a
+//        hit append j | row << 26 | skin << 31 at the list tail +
+//        popc(ballot & lanemask_lt), so every row's entries stay in ascending
+//        order inside the list; fwalk = n_front | flags.  The in-block j < i
+//        entries are not stored -- they are exactly the transposes of the
+//        block's front entries (unwalk restores them).  No atomics: the full
+//        row length n_front + n_back is bounded by n_front + the length of the
+//        cut-out index ranges; only a row whose bound exceeds max_neighbors
+//        walks its cut-out ranges (cut_hits) to count n_back exactly for the
+//        overflow check.
 // predicated select (keeps the compiler from branching on small selects)
 __device__ __forceinline__ float fsel(bool p, float a, float b) {
     float r;
@@ -1015,8 +1022,31 @@ constexpr int RB_BLOCK = 32 * DPDB_FORCE_TPW * DPDB_FORCE_WARPS;  // == FORCE_BL
 #endif
 constexpr int RB_THREADS = DPDB_RB_THREADS;  // lanes per CTA (RB_BLOCK / RB_THREADS passes)
 constexpr int RB_SLOTS = 29;     // 27 stencil cells + one split by the cut-out + a trash slot
-constexpr size_t RB_SMEM = (size_t)RB_SLOTS * RB_THREADS * 6 + RB_BLOCK * 4;
+constexpr size_t RB_SMEM = (size_t)RB_SLOTS * RB_THREADS * 6;
 constexpr uint32_t RB_NONE = 0xFFFFFFFFu;
+
+// Rows whose front count + cut-out length could exceed max_neighbors: the
+// exact number of in-block j < i within r_c + skin (the row's back entries),
+// the builder's own fp32 test over every stencil cell's [max(start, b0), i).
+__device__ __noinline__ uint32_t cut_hits(const float4* __restrict__ pos4, const uint32_t* __restrict__ stencil,
+                                          uint32_t ns, const uint32_t* __restrict__ cell_start, uint32_t i,
+                                          uint32_t b0, float4 pi, uint32_t wfl, float3 L, float3 H, float cut_s) {
+    uint32_t n = 0;
+    for (uint32_t s = 0; s < ns; ++s) {
+        const uint32_t c = stencil[s];
+        const uint32_t st = max(cell_start[c], b0), en = min(cell_start[c + 1], i);
+        for (uint32_t j = st; j < en; ++j) {
+            const float4 pj = pos4[j];
+            float dx = __fsub_rn(pi.x, pj.x), dy = __fsub_rn(pi.y, pj.y), dz = __fsub_rn(pi.z, pj.z);
+            if (wfl & 1u) dx = min_image_f(dx, L.x, H.x);
+            if (wfl & 2u) dy = min_image_f(dy, L.y, H.y);
+            if (wfl & 4u) dz = min_image_f(dz, L.z, H.z);
+            const float d2 = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
+            n += d2 <= cut_s;
+        }
+    }
+    return n;
+}
 
 template <bool WALK, bool GH>
 __global__ void __launch_bounds__(RB_THREADS, 1024 / RB_THREADS) k_build_range(BuildArgs a) {
@@ -1024,15 +1054,12 @@ __global__ void __launch_bounds__(RB_THREADS, 1024 / RB_THREADS) k_build_range(B
     uint32_t(*rs)[RB_THREADS] = reinterpret_cast<uint32_t(*)[RB_THREADS]>(rb_smem);
     uint16_t(*rl)[RB_THREADS] =
         reinterpret_cast<uint16_t(*)[RB_THREADS]>(rb_smem + RB_SLOTS * RB_THREADS);
-    uint32_t* back = rb_smem + RB_SLOTS * RB_THREADS + RB_SLOTS * RB_THREADS / 2;
     const uint32_t t = threadIdx.x;
     const uint32_t b0 = blockIdx.x * RB_BLOCK;
     const uint32_t bn = min((uint32_t)RB_BLOCK, a.n_local - b0);
     const uint32_t bend = b0 + bn;
     const uint32_t maxn = a.maxn;
     __shared__ uint32_t ghost_seen;
-    if (WALK)
-        for (uint32_t q = t; q < RB_BLOCK; q += RB_THREADS) back[q] = 0;
     if (t == 0) ghost_seen = 0u;
     __syncthreads();
     uint32_t cnt[RB_BLOCK / RB_THREADS];  // nc | nsk << 16 per pass
@@ -1074,7 +1101,7 @@ __global__ void __launch_bounds__(RB_THREADS, 1024 / RB_THREADS) k_build_range(B
         const uint32_t cut_lo = WALK ? b0 : i;  // excluded index range [cut_lo, i]
         const uint32_t* otab = a.ostart ? a.ostart : a.cell_start;
         const int osh = a.ostart ? 3 : 0;
-        uint32_t nr = 0;
+        uint32_t nr = 0, cutl = 0;
         const uint32_t* srow = a.stencil + (size_t)r * 32;
         const uint8_t* crow = a.stencil_code + (size_t)r * 32;
         bool big = false;
@@ -1121,6 +1148,10 @@ __global__ void __launch_bounds__(RB_THREADS, 1024 / RB_THREADS) k_build_range(B
                 // over the kept non-empty ones (slot RB_SLOTS - 1 absorbs the rest)
                 const bool keep = kp[q];
                 const uint32_t e1 = min(en[q], cut_lo), s2 = max(st[q], i + 1u);
+                if (WALK) {  // cut-out [max(st, b0), min(en, i)): the row's possible back entries
+                    const uint32_t c0 = max(st[q], cut_lo), c1 = min(en[q], i);
+                    cutl += keep && c1 > c0 ? c1 - c0 : 0u;
+                }
                 const uint32_t l1 = e1 > st[q] ? e1 - st[q] : 0u;
                 const uint32_t l2 = en[q] > s2 ? en[q] - s2 : 0u;
                 big |= keep && max(l1, l2) > 0xFFFFu;
@@ -1162,7 +1193,6 @@ __global__ void __launch_bounds__(RB_THREADS, 1024 / RB_THREADS) k_build_range(B
         float4 p0 = __ldg(a.pos4 + j0), p1 = __ldg(a.pos4 + j1);
         uint32_t* rowp = a.entries + (size_t)(i & ~31u) * maxn + (i & 31u);
         uint32_t* wp = rowp;
-        const uint32_t back_sa = (uint32_t)__cvta_generic_to_shared(back) - 4u * b0;
         const int wstep = 32 - 31 * (int)maxn;  // entry 32q+31 -> 32(q+1)
         uint32_t kf = 0, kb = 0, nc = 0, nsk = 0;
         const float cut_s = a.cut_s, cut_c = a.cut_c;
@@ -1195,16 +1225,12 @@ __global__ void __launch_bounds__(RB_THREADS, 1024 / RB_THREADS) k_build_range(B
                 const bool core = d2 <= cut_c;
                 if (GH && hit && j >= a.n_local) ghost_seen = 1u;  // same value from every writer
                 if (WALK) {
-                    // predicated store / shared add (no branch per candidate)
+                    // predicated store into the tile-transposed scratch rows (no branch)
                     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.global.u32 [%0], %1;\n\t}"
                                  ::"l"(wp), "r"(core ? j : (j | 0x80000000u)),
                                  "r"((uint32_t)(hit && kf < maxn)));
                     wp += hit ? (((kf & 31u) == 31u) ? wstep : (int)maxn) : 0;
                     kf += hit;
-                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.shared.add.u32 [%0], %1;\n\t}"
-                                 ::"r"(back_sa + 4u * j), "r"(core ? 1u : 0x10000u),
-                                 "r"((uint32_t)(hit && j < bend && j > i))
-                                 : "memory");
                 } else {
                     const uint32_t k = core ? kf : maxn - 1u - kb;
                     if (hit && kf + kb < maxn) rowp[(k & 31u) * maxn + (k & ~31u)] = j;
@@ -1229,6 +1255,46 @@ __global__ void __launch_bounds__(RB_THREADS, 1024 / RB_THREADS) k_build_range(B
             walk(std::false_type{});
         cnt[pass] = min(nc, 0xFFFFu) | (min(nsk, 0xFFFFu) << 16);  // saturate: >= 65535 overflows maxn anyway
         kfs[pass] = kf;
+        if (WALK) {
+            // The tile's flat pair list for the force kernel: the warp's rows
+            // back-to-back in row order (exclusive warp scan of the row
+            // lengths), each item j | row << 26 | skin << 31.  The rows just
+            // written are read back coalesced (L1/L2 hits) and staged in this
+            // warp's columns of the range-list shared memory (free after the
+            // walk) so the list is written coalesced.
+            const uint32_t lane = t & 31u, wbase = t & ~31u;
+            const uint32_t kfc = min(kf, maxn);
+            uint32_t off = kfc;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, off, d);
+                if (lane >= (uint32_t)d) off += y;
+            }
+            const uint32_t tot = __shfl_sync(0xFFFFFFFFu, off, 31);
+            off -= kfc;
+            const uint32_t maxkf = __reduce_max_sync(0xFFFFFFFFu, kfc);
+            const uint32_t rowbits = lane << 26;
+            uint32_t* tl = a.plist + (size_t)(i & ~31u) * maxn;
+            constexpr uint32_t STG = RB_SLOTS * 32;  // staging words per warp
+            __syncwarp();
+            for (uint32_t c0 = 0; c0 < tot; c0 += STG) {
+                for (uint32_t m = 0; m < maxkf; ++m) {
+                    const uint32_t e = rowp[(m & 31u) * maxn + (m & ~31u)];
+                    const uint32_t q = off + m - c0;  // wraps (large) below the round
+                    if (m < kfc && q < STG) rs[q >> 5][wbase + (q & 31u)] = (e & 0x83FFFFFFu) | rowbits;
+                }
+                __syncwarp();
+                const uint32_t len = min(tot - c0, STG);
+                for (uint32_t q = lane; q < len; q += 32) tl[c0 + q] = rs[q >> 5][wbase + (q & 31u)];
+                __syncwarp();
+            }
+        }
+        if (WALK && row && kf + cutl > maxn) {  // the bound cannot rule out an overflow: count exactly
+            const uint32_t nb = cut_hits(a.pos4, a.stencil + (size_t)r * 32, ns, a.cell_start, i, b0, pi, wfl,
+                                         make_float3(a.L[0], a.L[1], a.L[2]),
+                                         make_float3(a.H[0], a.H[1], a.H[2]), a.cut_s);
+            if (kf + nb > maxn) raise_err(a.err, DPDB_EPHYSICS, EW_OVERFLOW, __float_as_uint(pi.w), kf + nb);
+        }
     }
     __syncthreads();
     if (t == 0 && a.blk_ghost) a.blk_ghost[blockIdx.x] = ghost_seen ? 1 : 0;
@@ -1236,18 +1302,16 @@ __global__ void __launch_bounds__(RB_THREADS, 1024 / RB_THREADS) k_build_range(B
     for (int pass = 0; pass < RB_BLOCK / RB_THREADS; ++pass) {
         const uint32_t i = b0 + pass * RB_THREADS + t;
         if (i >= bend) break;
-        uint32_t nc = cnt[pass] & 0xFFFFu, nsk = cnt[pass] >> 16;
-        if (WALK) {
-            const uint32_t bk = back[i - b0];
-            nc += bk & 0xFFFFu;
-            nsk += bk >> 16;
-        }
+        const uint32_t nc = cnt[pass] & 0xFFFFu, nsk = cnt[pass] >> 16;
         const uint32_t r = min(a.keys[i] >> a.key_shift, a.n_local_cells - 1u);
         const uint32_t ff = (a.cell_flags[r] >> 3) & 7u;
+        if (WALK) {  // counts of the full rows are formed on export (unwalk)
+            a.fwalk[i] = min(kfs[pass], maxn) | (ff << 26);
+            continue;
+        }
         if (nc + nsk > maxn)
             raise_err(a.err, DPDB_EPHYSICS, EW_OVERFLOW, __float_as_uint(a.pos4[i].w), nc + nsk);
         a.counts[i] = min(nc, 8191u) | (min(nsk, 8191u) << 13) | (ff << 26);
-        if (WALK) a.fwalk[i] = min(kfs[pass], maxn) | (ff << 26);
     }
 }
 
