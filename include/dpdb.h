@@ -19,6 +19,12 @@
  *   verlet_step / apply_body_force    SPEC.md:488-505 (impl. not shipped)
  *   compute_temperature               inc/core.hpp:116 (src/core.cpp:141-149)
  *
+ * The reference's own declarations (same signatures and types, compiled
+ * against its unmodified headers) are implemented over this ABI in dropin/:
+ * src/cell_grid.cpp and src/radix_sort.cpp are replaced, the missing
+ * src/neighbor_table.cpp, src/forces.cpp and src/integrate.cpp slots are
+ * filled.
+ *
  * Conventions (mirroring the reference's):
  *   - return 0 on success, otherwise the reference ErrorCategory value
  *     (inc/error.hpp:8-13): 1 config, 2 physics, 3 protocol, 4 io; plus
@@ -108,6 +114,17 @@ int dpdb_grid(const dpdb_ctx* ctx, dpdb_grid_info* out);
 int dpdb_grid_ranks(const dpdb_ctx* ctx, uint32_t* rank_of_cell);
 /* CUDA stream of the context (cudaStream_t) for interop */
 void* dpdb_stream(dpdb_ctx* ctx);
+/* CellGrid::make (inc/cell_grid.hpp:39-43, src/cell_grid.cpp:16-95) on the
+ * host, no device involved: the cell geometry of the slab [slab_lo, slab_hi)
+ * of a dims decomposition at coords (slab_lo/slab_hi/dims/coords all NULL:
+ * the single-domain grid over the box), cells >= cell_target per axis,
+ * 2^sub_bits sub-cells per axis.  ghost_lo/ghost_hi (may be NULL) receive the
+ * ghost layers; rank_of_cell may be NULL (size: out->n_total_cells).  The
+ * same grid every context on that box builds. */
+int dpdb_grid_plan(const dpdb_box* box, const double slab_lo[3], const double slab_hi[3],
+                   const int32_t dims[3], const int32_t coords[3], double cell_target,
+                   int32_t sub_bits, dpdb_grid_info* out, int32_t ghost_lo[3], int32_t ghost_hi[3],
+                   uint32_t* rank_of_cell);
 
 /* ------------------------------------------------------- state transfer */
 /* ParticleStore SoA, inc/core.hpp:29-47.  species/molecule may be NULL. */
@@ -166,6 +183,19 @@ int dpdb_tile_transpose(dpdb_ctx* ctx);
  * the layout flags (NeighborTable::tiled/joined, inc/neighbor_table.hpp:22-23). */
 int dpdb_get_neighbors(dpdb_ctx* ctx, uint32_t* entries, uint16_t* core, uint16_t* skin,
                        int32_t* tiled, int32_t* joined);
+/* import a neighbor table (NeighborTable, inc/neighbor_table.hpp:18-40) for
+ * the current particle order: entries[n_rows_pad * max_neighbors] in the
+ * given layout (tiled / joined flags), core/skin counts per row.  The next
+ * dpdb_compute_forces evaluates exactly these rows (the reference's
+ * compute_forces(store, table, ...) contract). */
+int dpdb_set_neighbors(dpdb_ctx* ctx, const uint32_t* entries, const uint16_t* core,
+                       const uint16_t* skin, int32_t tiled, int32_t joined);
+/* join_core_skin (op 0) / tile_transpose (op 1) of a caller-owned table
+ * (inc/neighbor_table.hpp:49-55) on the device, in place:
+ * entries[round_up(n_rows, 32) * max_neighbors] in the layout given by
+ * tiled / joined, counts per row.  No context needed. */
+int dpdb_table_layout(int device, int op, size_t n_rows, uint32_t max_neighbors, uint32_t* entries,
+                      const uint16_t* core, const uint16_t* skin, int32_t tiled, int32_t joined);
 /* per-particle signatures from the current fp64 velocities */
 int dpdb_signatures(dpdb_ctx* ctx, uint32_t* sig);
 /* compute_forces + bond_forces + apply_body_force with step_mix(seed, step) */

@@ -66,6 +66,11 @@ SYMBOLS = {
     "dpdb_destroy": (C.c_int, [C.c_void_p]),
     "dpdb_grid": (C.c_int, [C.c_void_p, C.POINTER(GridInfo)]),
     "dpdb_grid_ranks": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "dpdb_grid_plan": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
+                                 C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "dpdb_set_neighbors": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32]),
+    "dpdb_table_layout": (C.c_int, [C.c_int, C.c_int, C.c_size_t, C.c_uint32, C.c_void_p, C.c_void_p,
+                                    C.c_void_p, C.c_int32, C.c_int32]),
     "dpdb_stream": (C.c_void_p, [C.c_void_p]),
     "dpdb_upload": (C.c_int, [C.c_void_p, C.c_size_t] + [C.c_void_p] * 9),
     "dpdb_upload_forces": (C.c_int, [C.c_void_p] + [C.c_void_p] * 3),

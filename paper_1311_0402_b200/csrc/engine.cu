@@ -1077,6 +1077,45 @@ int dpdb_grid_ranks(const dpdb_ctx* ctx, uint32_t* rank_of_cell) {
 
 void* dpdb_stream(dpdb_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
 
+int dpdb_grid_plan(const dpdb_box* box, const double slab_lo[3], const double slab_hi[3],
+                   const int32_t dims[3], const int32_t coords[3], double cell_target,
+                   int32_t sub_bits, dpdb_grid_info* o, int32_t ghost_lo[3], int32_t ghost_hi[3],
+                   uint32_t* rank_of_cell) {
+    if (!box || !o) return fail(nullptr, DPDB_ECONFIG, "grid_plan: null argument");
+    if (sub_bits < 0 || sub_bits > 4) return fail(nullptr, DPDB_ECONFIG, "grid_plan: sub_bits must be 0..4");
+    const int one[3] = {1, 1, 1}, zero[3] = {0, 0, 0};
+    int d3[3], c3[3];
+    double lo[3], hi[3];
+    for (int k = 0; k < 3; ++k) {
+        d3[k] = dims ? dims[k] : one[k];
+        c3[k] = coords ? coords[k] : zero[k];
+        lo[k] = slab_lo ? slab_lo[k] : box->lo[k];
+        hi[k] = slab_hi ? slab_hi[k] : box->hi[k];
+        if (d3[k] < 1 || c3[k] < 0 || c3[k] >= d3[k])
+            return fail(nullptr, DPDB_ECONFIG, "grid_plan: coords outside the decomposition");
+    }
+    HostGrid g;
+    std::string err;
+    const int rc = g.make(*box, lo, hi, d3, c3, cell_target, sub_bits, err);
+    if (rc) return fail(nullptr, rc, err);
+    for (int k = 0; k < 3; ++k) {
+        o->ncell[k] = g.ncell[k];
+        o->ncell_ext[k] = g.ncell_ext[k];
+        o->wrapmode[k] = g.wrap[k];
+        o->cell_size[k] = g.cell_size[k];
+        o->inv_cell[k] = g.inv_cell[k];
+        o->origin[k] = g.origin[k];
+        if (ghost_lo) ghost_lo[k] = g.ghost_lo[k];
+        if (ghost_hi) ghost_hi[k] = g.ghost_hi[k];
+    }
+    o->bits_per_axis = g.bits_per_axis;
+    o->key_bits = g.key_bits();
+    o->n_local_cells = g.n_local_cells;
+    o->n_total_cells = g.n_total_cells;
+    if (rank_of_cell) std::memcpy(rank_of_cell, g.rank_of_cell.data(), g.rank_of_cell.size() * 4);
+    return 0;
+}
+
 int dpdb_upload(dpdb_ctx* ctx, size_t n, const double* x, const double* y, const double* z,
                 const double* vx, const double* vy, const double* vz, const uint32_t* tag,
                 const uint8_t* species, const uint32_t* molecule) {
@@ -1632,6 +1671,71 @@ int dpdb_get_neighbors(dpdb_ctx* ctx, uint32_t* entries, uint16_t* core, uint16_
     if (tiled) *tiled = ctx->tiled;
     if (joined) *joined = ctx->joined;
     return 0;
+}
+
+int dpdb_set_neighbors(dpdb_ctx* ctx, const uint32_t* entries, const uint16_t* core,
+                       const uint16_t* skin, int32_t tiled, int32_t joined) {
+    TRY(require_ctx(ctx));
+    CK(cudaSetDevice(ctx->device));
+    const size_t n = ctx->n, rows = (n + 31) & ~(size_t)31, maxn = ctx->maxn;
+    if (n && (!entries || !core || !skin)) return fail(ctx, DPDB_ECONFIG, "set_neighbors: null array");
+    std::vector<uint32_t> cnt(n);
+    for (size_t i = 0; i < n; ++i) {
+        if ((uint32_t)core[i] + skin[i] > maxn)
+            return fail(ctx, DPDB_ECONFIG, "set_neighbors: row longer than max_neighbors");
+        cnt[i] = core[i] | ((uint32_t)skin[i] << 13);
+    }
+    // the force kernels apply the minimum image through the posq frame: no per-row flags needed
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (n) {
+        CK(cudaMemcpy(ctx->entries, entries, rows * maxn * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->counts, cnt.data(), n * 4, cudaMemcpyHostToDevice));
+    }
+    ctx->tiled = tiled != 0;
+    ctx->joined = joined != 0;
+    ctx->walk = 0;
+    ctx->have_table = true;
+    return 0;
+}
+
+int dpdb_table_layout(int device, int op, size_t n_rows, uint32_t maxn, uint32_t* entries,
+                      const uint16_t* core, const uint16_t* skin, int32_t tiled, int32_t joined) {
+    dpdb_ctx* ctx = nullptr;  // CK/CKL report through the thread's error slot
+    if (op != 0 && op != 1) return fail(nullptr, DPDB_ECONFIG, "table_layout: op must be 0 (join) or 1 (transpose)");
+    if (maxn == 0 || maxn % 32) return fail(nullptr, DPDB_ECONFIG, "table_layout: max_neighbors must be a multiple of 32");
+    if (!n_rows) return 0;
+    if (!entries || (op == 0 && (!core || !skin))) return fail(nullptr, DPDB_ECONFIG, "table_layout: null array");
+    if (op == 0 && joined) return 0;
+    const int nd = dpdb_device_count();
+    if (nd <= 0 || device < 0 || device >= nd)
+        return fail(nullptr, DPDB_EDEVICE, "no compute capability 10.x device (the engine has no CPU fallback)");
+    CK(cudaSetDevice(device));
+    const size_t rows = (n_rows + 31) & ~(size_t)31;
+    uint32_t *d_e = nullptr, *d_c = nullptr;
+    CK(cudaMalloc(&d_e, rows * maxn * 4));
+    int rc = 0;
+    if (op == 0) {
+        std::vector<uint32_t> cnt(n_rows);
+        for (size_t i = 0; i < n_rows; ++i) cnt[i] = core[i] | ((uint32_t)skin[i] << 13);
+        if (cudaMalloc(&d_c, n_rows * 4) != cudaSuccess ||
+            cudaMemcpy(d_c, cnt.data(), n_rows * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+            rc = fail(nullptr, DPDB_EDEVICE, "table_layout: device allocation");
+    }
+    if (!rc && cudaMemcpy(d_e, entries, rows * maxn * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+        rc = fail(nullptr, DPDB_EDEVICE, "table_layout: copy in");
+    if (!rc) {
+        if (op == 0)
+            dpdb::k_join<<<blocks_for(n_rows, 256), 256>>>(d_e, d_c, (uint32_t)n_rows, maxn, tiled != 0);
+        else
+            dpdb::k_tile_transpose<<<dim3(maxn / 32, (unsigned)(rows / 32)), dim3(32, 8)>>>(d_e, (uint32_t)rows, maxn);
+        if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess ||
+            cudaMemcpy(entries, d_e, rows * maxn * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+            rc = fail(nullptr, DPDB_EDEVICE, "table_layout: kernel");
+    }
+    cudaFree(d_e);
+    if (d_c) cudaFree(d_c);
+    (void)ctx;
+    return rc;
 }
 
 int dpdb_signatures(dpdb_ctx* ctx, uint32_t* sig) {
