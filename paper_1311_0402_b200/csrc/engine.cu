@@ -87,7 +87,7 @@ struct dpdb_ctx {
     uint4* ang_rec{};
     float *ang_k{}, *ang_t0{};
     size_t n_bonds = 0;  // bonded terms present: bonds + angles
-    bool styled = false;  // FENE bonds or angles: k_bonds after the pair kernel, no fusion
+    bool styled = false;  // FENE bonds or angles present (bond styles / angle CSR uploaded)
     uint32_t max_tag = 0;
     // host copies of the topology (both CSRs are rebuilt when either changes)
     std::vector<uint32_t> h_bi, h_bj, h_aa, h_ab, h_ac;
@@ -98,7 +98,6 @@ struct dpdb_ctx {
     bool multi = false;  // n_species > 1: species packed into pos4.w bits 28-31
     bool no_fuse = false;  // DPDB_FUSE=0: keep the Verlet pass a separate kernel (A/B)
     uint32_t num_sms = 148;   // multiprocessors of the device
-    uint32_t swz_group = 0;   // force-block swizzle group (DPDB_SWZ; 0 = identity)
     // per-step thermo (dpdb_step_thermo): block partials of the phase-2 pass
     // and the records, written by the device straight into mapped pinned memory
     double* thermo_part{};
@@ -622,10 +621,11 @@ void force_dispatch_layout(dpdb_ctx* ctx, const dpdb::ForceArgs& a, bool body, i
 
 // Whether the step loop may run the next Verlet pass inside the force kernel:
 // single domain, walk layout with 128-slot rows (the walk kernel adds the
-// harmonic bond forces in its epilogue, so those fuse too; FENE / angles do not).
+// bonded terms -- harmonic / FENE bonds and harmonic angles -- in its
+// epilogue, so bonded systems fuse too).
 bool can_fuse(const dpdb_ctx* ctx) {
     return ctx->walk && ctx->maxn == 128 && !ctx->md_valid &&
-           ctx->dims[0] * ctx->dims[1] * ctx->dims[2] == 1 && !ctx->no_fuse && !ctx->styled;
+           ctx->dims[0] * ctx->dims[1] * ctx->dims[2] == 1 && !ctx->no_fuse;
 }
 
 // fuse (step loop only, can_fuse): FUSE_STREAMS / FUSE_KEYS run phase 2 of
@@ -698,15 +698,12 @@ int do_forces(dpdb_ctx* ctx, uint32_t step, int fuse = dpdb::FUSE_NONE, bool the
         a.tg[q] = (float)p.gamma[q];
         a.ts[q] = (float)(ctx->sigma[q] / std::sqrt(p.dt));
     }
-    // harmonic bonds ride in the walk kernel's epilogue; FENE and angles need k_bonds
-    const bool bonds_after = ctx->n_bonds && (!ctx->walk || ctx->styled);
+    // bonded terms ride in the walk kernel's epilogue; the reference-layout kernel needs k_bonds
+    const bool bonds_after = ctx->n_bonds && !ctx->walk;
     if (ctx->n_bonds && !bonds_after) {
         a.has_bonds = 1;
         a.bd = bond_args(ctx);
     }
-    a.n_blocks = (uint32_t)((ctx->n + dpdb::FORCE_BLOCK - 1) / dpdb::FORCE_BLOCK);
-    a.swz_group = ctx->swz_group;
-    a.swz_sms = ctx->num_sms;
     if (part >= 0) {
         a.blk_sel = ctx->blk_ghost;
         a.sel_val = (uint32_t)part;
@@ -858,7 +855,6 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         int sms = 0;
         if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0)
             ctx->num_sms = (uint32_t)sms;
-        if (const char* z = std::getenv("DPDB_SWZ")) ctx->swz_group = (uint32_t)std::atoi(z);
     }
     for (int q = 0; q < ns * ns; ++q) ctx->sigma[q] = std::sqrt(2.0 * params->gamma[q] * params->kbt);
     std::string err;

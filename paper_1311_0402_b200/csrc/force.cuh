@@ -43,10 +43,8 @@ struct ForceArgs {
     // boundary split around the ghost update); null = every block
     const uint8_t* blk_sel;
     uint32_t sel_val;
-    // block swizzle (block_of_cta): consecutive force blocks -- Morton
-    // neighbors sharing most of their halo -- on the same SM at the same time
-    uint32_t swz_group, swz_sms, n_blocks;
-    // k_force_walk<GENERAL>: harmonic bonds added in the epilogue (else k_bonds runs after)
+    // k_force_walk<GENERAL>: the bonded terms (harmonic / FENE bonds, harmonic
+    // angles) added in the epilogue (else k_bonds runs after the pair kernel)
     int has_bonds;
     BondArgs bd;
 };
@@ -446,26 +444,15 @@ constexpr bool FW_UNCOND = DPDB_FW_UNCOND;
 constexpr bool FW_PREFETCH = DPDB_FW_PREFETCH;  // A/B switch: L1 prefetch of vel4[j] in phase A
 constexpr int FW_Q = 160;  // < 32 leftovers + 4 x 32 hits per group
 
-// CTA -> force block.  The hardware deals CTAs round robin over the SMs, so
-// the CTAs resident together on one SM (c, c + S, c + 2S, ...) would own
-// blocks far apart in Morton order; this maps them to G consecutive blocks
-// instead, whose halos overlap, so their neighbor gathers share L1 lines.
-// Identity on the last partial wave and when G = 0.
-__device__ __forceinline__ uint32_t block_of_cta(const ForceArgs& a, uint32_t c) {
-    const uint32_t G = a.swz_group, W = G * a.swz_sms;
-    if (G == 0u || c >= a.n_blocks / W * W) return c;
-    const uint32_t w = c / W, r = c - w * W;
-    return w * W + (r % a.swz_sms) * G + r / a.swz_sms;
-}
-
 template <bool GENERAL, bool BODY, int MAXN, int FUSE>
-__global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceArgs a) {
+__global__ void __launch_bounds__(FORCE_WARPS * 32, GENERAL ? 32 / FORCE_WARPS : FW_MINB)
+    k_force_walk(ForceArgs a) {  // GENERAL (species tables, bonded epilogue): 64 registers
     static_assert(FORCE_TPW % 2 == 0, "tiles are dealt in snake order, two per round");
     __shared__ uint32_t q_j[FORCE_WARPS][FW_Q];  // plist items: j | owner row << 26 | skin << 31
     __shared__ int4 own_p[FORCE_WARPS][32];
     __shared__ float4 own_v[FORCE_WARPS][32];
     __shared__ int acc[FORCE_BLOCK * 3];
-    const uint32_t blk = block_of_cta(a, blockIdx.x);
+    const uint32_t blk = blockIdx.x;
     if (a.blk_sel && a.blk_sel[blk] != a.sel_val) return;  // whole CTA
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t b0 = blk * FORCE_BLOCK;
@@ -626,7 +613,7 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FW_MINB) k_force_walk(ForceA
     for (int q = 0; q < PER_T; ++q) {
         const uint32_t t = threadIdx.x + q * FORCE_WARPS * 32;
         bset[q] = GENERAL && a.has_bonds && t < bn &&
-                  bond_force<false>(a.bd, b0 + t, bf[q][0], bf[q][1], bf[q][2]);
+                  bond_force<true>(a.bd, b0 + t, bf[q][0], bf[q][1], bf[q][2]);
     }
     if (FUSE != FUSE_NONE) {
 #pragma unroll
