@@ -9,13 +9,15 @@ table 2.1 GB) are far larger than the 126 MB L2, so no explicit L2 flush.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-Under torchrun (N > 1) the box is decomposed into N bricks of 4M particles
-each (weak scaling: 2x1x1 / 2x2x1 / 2x2x2, periodic), one brick
-per GPU: halo update every step and migration + full halo every rebuild over
-the engine's own NCCL transport (grouped ncclSend/Recv per neighbor
-direction on the brick's stream).  Timed on the device with CUDA events, max
-over ranks; rank 0 prints one JSON line.  --mode replicas runs N independent
-4M boxes instead.
+Under torchrun (N > 1) the box is decomposed into N bricks of C5's
+16,777,216 particles each (BASELINE.json configs[4], weak scaling, SURVEY
+8(e): 2x1x1 / 2x2x1 / 2x2x2, periodic), one brick per GPU: halo update every
+step and migration + full halo every rebuild over the engine's own NCCL
+transport (grouped ncclSend/Recv per neighbor direction on the brick's
+stream).  Timed on the device with CUDA events, max over ranks; rank 0 prints
+one JSON line.  The N = 1 line (C3, the roofline config) also carries
+`weak_scaling_base`: the same 16M-particle C5 brick on one GPU, the base the
+N > 1 values scale from.  --mode replicas runs N independent C3 boxes instead.
 """
 from __future__ import annotations
 
@@ -36,12 +38,13 @@ sys.path.insert(0, ROOT)
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 UNIT = "M particle-steps/s"
 N_C3 = 2**22
+N_C5 = 2**24  # weak-scaling particles per GPU (BASELINE.json configs[4])
 RHO = 3.0
 FALLBACK_HBM = 6650.0
 
 
-def c3_box():
-    L = (N_C3 / RHO) ** (1.0 / 3.0)
+def c3_box(n=N_C3):
+    L = (n / RHO) ** (1.0 / 3.0)
     return L
 
 
@@ -68,18 +71,48 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled during the timed region: NVML polled
+    every millisecond from a thread (the timed region of a short run lasts
+    tens of milliseconds), nvidia-smi -lms 50 when NVML is unavailable."""
 
     FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
               "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
               "clocks_event_reasons.sw_power_cap", "power.draw"]
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, gpu_index):
         self.idx = gpu_index
         self.proc = None
         self.lines = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons set)
+        self.nvml = None
 
     def __enter__(self):
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.idx)
+            bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap}
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            self.stop = threading.Event()
+
+            def poll():
+                while not self.stop.is_set():
+                    sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                    r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((float(sm), float(mx), {k for k, v in bits.items() if r & v}))
+                    time.sleep(0.001)
+
+            self.nvml = N
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:  # noqa: BLE001 -- fall back to nvidia-smi
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + ",".join(self.FIELDS),
@@ -96,6 +129,10 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        if self.nvml is not None:
+            self.stop.set()
+            self.t.join(timeout=1)
+            return
         if self.proc:
             time.sleep(0.12)
             self.proc.terminate()
@@ -106,7 +143,10 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for a, b, r in self.samples:
+            sm.append(a)
+            mx.append(b)
+            reasons |= r
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
@@ -116,13 +156,13 @@ class ClockSampler:
                 mx.append(float(parts[1]))
             except ValueError:
                 continue
-            for nm, val in zip(names, parts[2:6]):
+            for nm, val in zip(self.NAMES, parts[2:6]):
                 if val.lower().startswith("active"):
                     reasons.add(nm)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvml" if self.samples else "nvidia-smi"}
 
 
 def dist_init():
@@ -161,43 +201,84 @@ def max_over_ranks(x, ws, local):
 
 
 # ------------------------------------------------------------- CPU arms
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_sample(state, L, max_seconds=25.0, nthreads=None):
-    """The oracle's whole-step CPU driver (Alg. 1) on the same C3 system:
-    times up to 10 consecutive steps (step 10 is a rebuild) within max_seconds."""
+    """The reference CPU path timed per BASELINE.md section 2 on this host:
+    the oracle rebuilt here with -O3 -march=native -ffp-contract=off, every
+    host core (OpenMP + the reference's WorkerPool); the reorder step runs the
+    reference's OWN shipped reorder_particles / RadixSorter / cell list
+    (oracle/_ref), the neighbor build and forces the oracle's restatement (the
+    reference ships none).  10 warm-up steps, then repetitions of one rebuild
+    period (10 steps) -- 5, or as many as fit max_seconds -- and the median.
+    Returns the full-step rate (M particle-steps/s) and a details dict with
+    the force + neighbor rate (force every step + the build amortised over
+    the period) and the per-stage seconds."""
+    import tempfile
+
     import oracle as O
 
     nthreads = nthreads or len(os.sched_getaffinity(0))
+    wd = tempfile.mkdtemp(prefix="dpdb_cpu_")
+    native = O.use_native_build(wd)
     obox = O.make_box((0, 0, 0), (L, L, L))
     sim = O.Sim(obox, O.make_params(), tuple(state), nthreads=nthreads)
-    times = []
-    t_start = time.perf_counter()
-    while len(times) < 10 and time.perf_counter() - t_start < max_seconds:
-        t0 = time.perf_counter()
-        sim.run(1)
-        times.append(time.perf_counter() - t0)
+    ref_reorder = sim.use_reference_reorder(obox, 1.3, nthreads)
     n = len(state[0])
-    if len(times) == 10:  # 9 plain steps + 1 rebuild step = exactly one rebuild period
-        per_step = sum(times) / 10
-        sample = f"C3 {n} particles, steps 1-10 (one rebuild period), oracle port"
-    else:
-        per_step = sum(times) / len(times)
-        sample = f"C3 {n} particles, steps 1-{len(times)} (no rebuild in sample), oracle port"
-    return n / per_step / 1e6, nthreads, sample, len(times)
+    t_start = time.perf_counter()
+    sim.run(10)  # warm-up (includes a rebuild)
+    sim.stage_seconds(reset=True)
+    warm = time.perf_counter() - t_start
+    reps = []
+    budget = max(max_seconds - warm, 0.0)
+    while len(reps) < 5:
+        t0 = time.perf_counter()
+        sim.run(10)
+        wall = time.perf_counter() - t0
+        st = sim.stage_seconds(reset=True)
+        reps.append((wall, st))
+        if time.perf_counter() - t_start - warm + wall > budget:
+            break
+    walls = [w for w, _ in reps]
+    fn = [st[2] + st[3] for _, st in reps]  # build + forces per period
+    full = n * 10 / statistics.median(walls) / 1e6
+    forcenb = n * 10 / statistics.median(fn) / 1e6
+    stages = np.median(np.array([st for _, st in reps]), axis=0) / 10
+    details = {"force_neighbor": round(forcenb, 4),
+               "stage_s_per_step": {k: round(float(v), 5) for k, v in
+                                    zip(["integrate", "reorder", "build", "forces"], stages)},
+               "reps": len(reps), "cpu_model": cpu_model(),
+               "build": ("oracle -O3 -march=native -ffp-contract=off (built on this host)" if native
+                         else "prebuilt oracle -O3 -march=x86-64-v3"),
+               "reorder": ("reference's shipped reorder_particles + RadixSorter (oracle/_ref)"
+                           if ref_reorder else "oracle restatement")}
+    sample = (f"{n} particles: 10 warm-up steps, median of {len(reps)} x 10 steps (one rebuild "
+              f"period each); full step {full:.3f}, force+neighbor {forcenb:.3f} M particle-steps/s")
+    return full, nthreads, sample, len(reps) * 10, details
 
 
 def run_reference(args, ws, rank):
     if rank != 0:
         return
-    L = c3_box()
-    state = synth_state(N_C3, L)
-    val, cores, sample, nsteps = cpu_sample(state, L, max_seconds=float(args.ref_seconds))
+    NP = N_C5 if ws > 1 and args.mode == "bricks" else N_C3  # our arm's per-GPU workload
+    L = c3_box(NP)
+    state = synth_state(NP, L)
+    val, cores, sample, nsteps, det = cpu_sample(state, L, max_seconds=float(args.ref_seconds))
     line = {
         "impl": "reference", "metric": METRIC, "value": round(val, 4), "unit": UNIT,
-        "n_gpus": args.gpus, "steps": nsteps, "warmup": 0, "ms_per_step": N_C3 / (val * 1e6) * 1e3,
+        "n_gpus": args.gpus, "steps": nsteps, "warmup": 0, "ms_per_step": NP / (val * 1e6) * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": config_dict(ws, args.mode),
         "cpu_baseline": {"value": round(val, 4), "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, **det},
         "e2e": {"value": round(val, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -223,12 +304,45 @@ def config_dict(ws, mode="bricks"):
     if ws > 1:
         par = (f"bricks{'x'.join(map(str, brick_dims(ws)))}" if mode == "bricks"
                else f"replicas{ws}")
+    if ws > 1 and mode == "bricks":
+        return {"workload": "C5: weak-scaling homogeneous DPD fluid, 16,777,216 particles per GPU, "
+                            "rho=3, L=177.5 per GPU brick, a=25, gamma=4.5, kT=1, rc=1, dt=0.01, "
+                            "skin=0.3, rebuild=10",
+                "particles_per_gpu": N_C5, "rho": RHO, "rebuild_every": 10, "max_neighbors": 128,
+                "parallelism": par,
+                "l2": "inputs > L2 (2.8 GB state + 17 GB tables per GPU vs 126 MB L2); no flush"}
     return {"workload": "C3: homogeneous DPD fluid, 4,194,304 particles per GPU, rho=3, "
                         "L=111.818 per GPU, a=25, gamma=4.5, kT=1, rc=1, dt=0.01, skin=0.3, "
                         "rebuild=10",
             "particles_per_gpu": N_C3, "rho": RHO, "rebuild_every": 10, "max_neighbors": 128,
             "parallelism": par,
-            "l2": "inputs > L2 (0.7 GB state + 2.1 GB table vs 126 MB L2); no flush"}
+            "l2": "inputs > L2 (0.7 GB state + 4.3 GB tables vs 126 MB L2); no flush"}
+
+
+def warm_clocks(e, ws, seconds=2.0):
+    """Untimed extra warm-up steps until `seconds` of device work have run: an
+    idle B200 parks its SM clock (~120 MHz) and a few milliseconds of warm-up
+    steps time a clock ramp, not the kernels (measured: 5x slower force stage
+    on a freshly acquired box).  The step count is agreed across ranks."""
+    import torch
+
+    t0 = time.perf_counter()
+    k = 0
+    while True:
+        e.step(10)
+        torch.cuda.synchronize()
+        k += 10
+        done = time.perf_counter() - t0 >= seconds
+        if ws == 1:
+            if done:
+                return k
+        else:
+            import torch.distributed as dist
+
+            flag = torch.tensor([1.0 if done else 0.0], device="cuda")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if flag.item() > 0:
+                return k
 
 
 # --------------------------------------------------------------- B200 arm
@@ -273,30 +387,32 @@ def run_b200(args, ws, rank, local):
     from paper_1311_0402_b200 import domain as D
 
     torch.cuda.set_device(local)
-    L = c3_box()
     params = dpd.PairParams()
     run = dpd.RunConfig()
     bricks = ws > 1 and args.mode == "bricks"
+    NP = N_C5 if bricks else N_C3  # particles per GPU
+    L = c3_box(NP)
     if bricks:
-        # weak scaling: N bricks of the C3 cube, one per GPU, 4M particles each
+        # weak scaling (C5): N bricks of the 16M cube, one per GPU
         dims = brick_dims(ws)
         box = dpd.SimBox((0.0, 0.0, 0.0), tuple(L * d for d in dims))
         coords = D.coords_of(rank, dims)
         lo, hi = D.slab_bounds(box, dims, coords)
-        state = synth_state(N_C3, L, seed=2024 + rank)
+        state = synth_state(NP, L, seed=2024 + rank)
         for k in range(3):  # place this rank's particles inside its own slab
             state[k] = np.minimum(lo[k] + state[k] * ((hi[k] - lo[k]) / L),
                                   np.nextafter(hi[k], lo[k]))
-        state[6] = state[6] + np.uint32(rank * N_C3)
-        e = _BrickRunner(D.NcclBrick(box, params, run, dims, capacity=int(N_C3 * 1.2),
+        state[6] = state[6] + np.uint32(rank * NP)
+        e = _BrickRunner(D.NcclBrick(box, params, run, dims, capacity=int(NP * 1.2),
                                      device=local))
     else:
-        state = synth_state(N_C3, L, seed=2024 + rank)
+        state = synth_state(NP, L, seed=2024 + rank)
         box = dpd.SimBox((0.0, 0.0, 0.0), (L, L, L))
-        e = dpd.Engine(box, params, run, capacity=N_C3, device=local)
+        e = dpd.Engine(box, params, run, capacity=NP, device=local)
     e.upload(dpd.ParticleStore.from_arrays(*state))
     e.setup()
     e.step(args.warmup)
+    warm_clocks(e, ws)
     barrier_sync(ws)
     with ClockSampler(local) as clk:
         t0 = time.perf_counter()
@@ -306,7 +422,7 @@ def run_b200(args, ws, rank, local):
     ms_max = max_over_ranks(ms, ws, local)
     stats = e.table_stats()
     nbar = stats["mean_row"]
-    total_particles = N_C3 * ws
+    total_particles = NP * ws
     value = total_particles * args.steps / (ms_max * 1e-3) / 1e6
 
     # roofline of the dominant kernel (pair force): per particle
@@ -323,7 +439,7 @@ def run_b200(args, ws, rank, local):
             per.append(48.0)
         else:
             per.append(36.0 + 100.0 + (8.0 if (step + 1) % run.rebuild_every == 0 else 32.0))
-    bytes_per_launch = N_C3 * (float(np.mean(per)) + 4.0 * nbar)
+    bytes_per_launch = NP * (float(np.mean(per)) + 4.0 * nbar)
     achieved = bytes_per_launch / (force_launch_ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
     traffic = None
@@ -338,13 +454,13 @@ def run_b200(args, ws, rank, local):
                          "dram_throughput_pct": pj.get("dram_throughput_pct"),
                          "source": f"profiles/{pj.get('tag')}_ncu.md"}
     # full-step byte model (reported only): B = 48 + 4n + (16 + 4n)/R
-    step_bytes = N_C3 * (48.0 + 4.0 * nbar + (16.0 + 4.0 * nbar) / run.rebuild_every)
+    step_bytes = NP * (48.0 + 4.0 * nbar + (16.0 + 4.0 * nbar) / run.rebuild_every)
     step_ms = ms / args.steps
 
     # end to end through the public API with host buffers (pinned): upload,
     # setup, K steps with the per-step thermo read-back, download
     pinned = [torch.from_numpy(a).pin_memory().numpy() for a in state]
-    out = [torch.empty(N_C3, dtype=torch.float64).pin_memory().numpy() for _ in range(6)]
+    out = [torch.empty(NP, dtype=torch.float64).pin_memory().numpy() for _ in range(6)]
     def e2e_pass(k):
         e.upload(dpd.ParticleStore.from_arrays(*pinned))
         e.setup()
@@ -379,8 +495,8 @@ def run_b200(args, ws, rank, local):
     e2e_parts = {"upload": t_up - t0, "setup": t_setup - t_up, "steps": t_steps - t_setup,
                  "download": t_end - t_steps}
     e2e = total_particles * args.steps / e2e_s / 1e6
-    h2d = N_C3 * (6 * 8 + 4)
-    d2h_state = N_C3 * ((9 * 8 + 4 + 1 + 4) if bricks else 6 * 8)
+    h2d = NP * (6 * 8 + 4)
+    d2h_state = NP * ((9 * 8 + 4 + 1 + 4) if bricks else 6 * 8)
     d2h = d2h_state / args.steps + 40
 
     line = {
@@ -411,11 +527,27 @@ def run_b200(args, ws, rank, local):
         "clocks": clk.summary(),
         "wall_s_timed": round(wall, 4),
     }
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        val, cores, sample, _ = cpu_sample(state, L, max_seconds=float(args.ref_seconds))
-        line["cpu_baseline"] = {"value": round(val, 4), "unit": UNIT, "cores": cores,
-                                "kind": "port", "sample": sample}
     e.close()
+    if ws == 1 and not args.no_c5_base:
+        # the weak-scaling base: one C5 brick (16,777,216 particles) on this GPU
+        L5 = c3_box(N_C5)
+        e5 = dpd.Engine(dpd.SimBox((0.0, 0.0, 0.0), (L5, L5, L5)), params, run, capacity=N_C5,
+                        device=local)
+        e5.upload(dpd.ParticleStore.from_arrays(*synth_state(N_C5, L5, seed=2024)))
+        e5.setup()
+        e5.step(args.warmup)
+        warm_clocks(e5, 1, seconds=1.0)
+        ms5, _, _ = e5.step_timed(args.steps, stages=False)
+        e5.close()
+        line["weak_scaling_base"] = {
+            "workload": "C5 brick on one GPU: 16,777,216 particles, rho=3, L=177.5 (the per-GPU "
+                        "size of the N > 1 runs)",
+            "value": round(N_C5 * args.steps / (ms5 * 1e-3) / 1e6, 3), "unit": UNIT,
+            "ms_per_step": round(ms5 / args.steps, 5)}
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        val, cores, sample, _, det = cpu_sample(state, L, max_seconds=float(args.ref_seconds))
+        line["cpu_baseline"] = {"value": round(val, 4), "unit": UNIT, "cores": cores,
+                                "kind": "port", "sample": sample, **det}
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -427,6 +559,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c5-base", action="store_true", help="N = 1: skip the 16M weak-scaling base")
     ap.add_argument("--ref-seconds", default=25.0, type=float)
     ap.add_argument("--mode", default="bricks", choices=["bricks", "replicas"],
                     help="N > 1: brick decomposition over NCCL (default) or independent replicas")

@@ -332,6 +332,12 @@ int dpdb_group_step_thermo(dpdb_ctx* const* ctxs, int n_bricks, int64_t nsteps, 
 #define DPDB_NCCL_ID_BYTES 128
 int dpdb_nccl_unique_id(uint8_t id[DPDB_NCCL_ID_BYTES]);
 int dpdb_nccl_attach(dpdb_ctx* ctx, const uint8_t id[DPDB_NCCL_ID_BYTES], int nranks, int rank);
+/* TEST transport: attach the nranks bricks of ONE process (one host thread
+ * per brick afterwards, each calling dpdb_dist_*) to an in-process stand-in
+ * of NCCL's grouped Send / Recv and AllGather (device copies, NCCL's
+ * per-peer ordering and completion semantics), so the NCCL driver's
+ * multi-rank call sequence runs on a single GPU. */
+int dpdb_nccl_mock_attach(dpdb_ctx* const* ctxs, int nranks);
 int dpdb_dist_setup(dpdb_ctx* ctx);
 int dpdb_dist_step(dpdb_ctx* ctx, int64_t nsteps);
 /* dpdb_dist_step recording this brick's per-step sums: sums[5 s + 0..4] =

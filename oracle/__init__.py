@@ -83,6 +83,28 @@ def lib():
     return _lib
 
 
+def use_native_build(workdir):
+    """CPU-baseline build recipe: compile the oracle
+    with -O3 -march=native -ffp-contract=off -fopenmp for THIS host into
+    workdir and make it the library of this process.  Returns the path, or
+    None (then the portable prebuilt liboracle.so stays in use)."""
+    global _lib
+    if _lib is not None:
+        return None
+    out = os.path.join(workdir, "liboracle_native.so")
+    cc = "/usr/bin/gcc" if os.path.exists("/usr/bin/gcc") else "gcc"
+    try:
+        subprocess.run([cc, "-O3", "-march=native", "-fPIC", "-std=c11", "-ffp-contract=off",
+                        "-fopenmp", "-shared", "-o", out, os.path.join(HERE, "dpd_oracle.c"), "-lm"],
+                       check=True, capture_output=True, timeout=120)
+    except (OSError, subprocess.SubprocessError):
+        return None
+    L = C.CDLL(out)
+    _declare(L)
+    _lib = L
+    return out
+
+
 def ref():
     """The reference's own compiled code, or None when it was never built."""
     global _ref
@@ -147,6 +169,8 @@ def _declare(L):
         "orc_sim_n": (sz, [C.c_void_p]),
         "orc_sim_get": (None, [C.c_void_p] + [C.c_void_p] * 10),
         "orc_sim_temperature": (d, [C.c_void_p]),
+        "orc_sim_set_reorder_hook": (i, [C.c_void_p, C.c_void_p, C.c_void_p]),
+        "orc_sim_stage_seconds": (None, [C.c_void_p, np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS"), i]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -178,6 +202,8 @@ def _declare_ref(R):
         "ref_temperature": (d, [sz, f64p, f64p, f64p]),
         "ref_minimum_image": (None, [f64p, f64p, f64p, i32x3, f64p]),
         "ref_params_sigma": (i, [i, f64p, f64p, d, d, d, d, f64p]),
+        "ref_sim_ctx_create": (C.c_void_p, [f64p, f64p, i32x3, d, i, C.c_uint]),
+        "ref_sim_ctx_destroy": (None, [C.c_void_p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(R, name)
@@ -350,6 +376,9 @@ class Sim:
         if getattr(self, "h", None):
             lib().orc_sim_destroy(self.h)
             self.h = None
+        if getattr(self, "_refctx", None):
+            ref().ref_sim_ctx_destroy(self._refctx)
+            self._refctx = None
 
     def run(self, nsteps):
         check(lib().orc_sim_run(self.h, nsteps))
@@ -368,3 +397,26 @@ class Sim:
 
     def temperature(self):
         return lib().orc_sim_temperature(self.h)
+
+    def use_reference_reorder(self, box, cell_target=1.3, workers=1):
+        """Run the reorder step with the reference's own shipped
+        reorder_particles + RadixSorter + cell list (oracle/_ref); False when
+        the reference build is absent."""
+        R = ref()
+        if R is None:
+            return False
+        lo = np.array(list(box.lo), np.float64)
+        hi = np.array(list(box.hi), np.float64)
+        per = np.array(list(box.periodic), np.int32)
+        self._refctx = R.ref_sim_ctx_create(lo, hi, per, cell_target, 2, workers)
+        if not self._refctx:
+            return False
+        fn = C.cast(R.ref_sim_reorder, C.c_void_p)
+        check(lib().orc_sim_set_reorder_hook(self.h, fn, self._refctx))
+        return True
+
+    def stage_seconds(self, reset=True):
+        """(integrate, reorder, build, forces) wall seconds since the last reset"""
+        out = np.zeros(4)
+        lib().orc_sim_stage_seconds(self.h, out, int(reset))
+        return out

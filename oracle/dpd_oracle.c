@@ -1009,6 +1009,12 @@ int orc_init_fluid(const orc_box* box, size_t n, double kbt, uint32_t seed, doub
  * velocity, forces with step_mix(seed, n), body force, phase2.
  * ==================================================================== */
 struct orc_sim {
+    /* CPU-baseline instrumentation: wall seconds per stage (integrate, reorder,
+     * build, forces) and an optional reorder hook (the reference's own shipped
+     * reorder_particles + cell list, oracle/ref_shim.cpp) */
+    double t_stage[4];
+    orc_reorder_hook hook;
+    void* hook_ctx;
     orc_box box;
     orc_params p;
     orc_grid g;
@@ -1025,7 +1031,22 @@ struct orc_sim {
     void* scratch;
 };
 
+static int sim_reorder_own(orc_sim* s);
 static int sim_reorder(orc_sim* s) {
+    const size_t n = s->n;
+    if (s->hook) {
+        double inner = 0.0;
+        const int rc = s->hook(s->hook_ctx, n, s->x, s->v, s->tag, s->species, s->cell_start, &inner);
+        s->t_stage[1] += inner;
+        return rc;
+    }
+    const double t0 = omp_get_wtime();
+    const int rc0 = sim_reorder_own(s);
+    s->t_stage[1] += omp_get_wtime() - t0;
+    return rc0;
+}
+
+static int sim_reorder_own(orc_sim* s) {
     const size_t n = s->n;
     int rc = orc_reorder_order(&s->g, n, s->x[0], s->x[1], s->x[2], s->order, NULL, s->nthreads);
     if (rc) return rc;
@@ -1152,20 +1173,42 @@ void orc_sim_destroy(orc_sim* s) {
 
 int orc_sim_run(orc_sim* s, int64_t nsteps) {
     for (int64_t t = 0; t < nsteps; ++t) {
+        double t0 = omp_get_wtime();
         int rc = orc_verlet_phase1(&s->box, s->p.dt, s->n, s->x[0], s->x[1], s->x[2], s->v[0],
                                    s->v[1], s->v[2], s->f[0], s->f[1], s->f[2], s->tag);
+        s->t_stage[0] += omp_get_wtime() - t0;
         if (rc) return rc;
         s->step += 1;
         if (s->step % s->rebuild_every == 0) {
             rc = sim_reorder(s);
-            if (!rc) rc = sim_build(s);
+            if (rc) return rc;
+            t0 = omp_get_wtime();
+            rc = sim_build(s);
+            s->t_stage[2] += omp_get_wtime() - t0;
             if (rc) return rc;
         }
+        t0 = omp_get_wtime();
         rc = sim_forces(s);
+        s->t_stage[3] += omp_get_wtime() - t0;
         if (rc) return rc;
+        t0 = omp_get_wtime();
         orc_verlet_phase2(s->p.dt, s->n, s->v[0], s->v[1], s->v[2], s->f[0], s->f[1], s->f[2]);
+        s->t_stage[0] += omp_get_wtime() - t0;
     }
     return ORC_OK;
+}
+
+int orc_sim_set_reorder_hook(orc_sim* s, orc_reorder_hook hook, void* ctx) {
+    s->hook = hook;
+    s->hook_ctx = ctx;
+    return ORC_OK;
+}
+
+void orc_sim_stage_seconds(orc_sim* s, double out[4], int reset) {
+    for (int k = 0; k < 4; ++k) {
+        out[k] = s->t_stage[k];
+        if (reset) s->t_stage[k] = 0.0;
+    }
 }
 
 int64_t orc_sim_step_index(const orc_sim* s) { return s->step; }

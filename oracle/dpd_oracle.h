@@ -180,6 +180,14 @@ orc_sim* orc_sim_create(const orc_box* box, const orc_params* p, double skin, in
                         const double* z, const double* vx, const double* vy, const double* vz,
                         const uint32_t* tag, const uint8_t* species, int nthreads);
 void orc_sim_destroy(orc_sim* s);
+/* reorder step replacement for the CPU baseline (the reference's own shipped
+ * reorder_particles, oracle/ref_shim.cpp ref_sim_reorder): permute x, v, tag,
+ * species in place, fill cell_start, report the seconds spent in *seconds */
+typedef int (*orc_reorder_hook)(void* ctx, size_t n, double* x[3], double* v[3], uint32_t* tag,
+                                uint8_t* species, uint32_t* cell_start, double* seconds);
+int orc_sim_set_reorder_hook(orc_sim* s, orc_reorder_hook hook, void* ctx);
+/* wall seconds per stage since the last reset: integrate, reorder, build, forces */
+void orc_sim_stage_seconds(orc_sim* s, double out[4], int reset);
 int orc_sim_run(orc_sim* s, int64_t nsteps);
 int64_t orc_sim_step_index(const orc_sim* s);
 size_t orc_sim_n(const orc_sim* s);

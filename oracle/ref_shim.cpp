@@ -4,7 +4,9 @@
 // oracle/_ref/libdpdref.so.  TEST INFRASTRUCTURE ONLY: it exists to pin the
 // C restatement in oracle/dpd_oracle.c and to generate tests/golden/.
 // No reference source is copied into this repository.
+#include <chrono>
 #include <cstdint>
+#include <memory>
 #include <cstring>
 #include <span>
 #include <string>
@@ -205,6 +207,63 @@ int ref_params_sigma(int n_species, const double* a, const double* gamma, double
             n_species, std::vector<double>(a, a + n_species * n_species),
             std::vector<double>(gamma, gamma + n_species * n_species), kbt, s, r_c, dt);
         std::memcpy(sigma, p.sigma.data(), p.sigma.size() * 8);
+    });
+}
+
+// ---- CPU baseline: the reference's own reorder step inside the oracle's
+// whole-step driver (orc_sim_set_reorder_hook).  One persistent grid,
+// WorkerPool and RadixSorter per run, as the reference's runner would hold.
+struct RefSimCtx {
+    dpd::SimBox box;
+    dpd::CellGrid grid;
+    std::unique_ptr<dpd::WorkerPool> pool;
+    dpd::RadixSorter sorter;
+    dpd::ParticleStore st;
+};
+
+void* ref_sim_ctx_create(const double lo[3], const double hi[3], const int32_t periodic[3],
+                         double cell_target, int sub_bits, unsigned workers) {
+    auto* c = new RefSimCtx();
+    if (guarded([&] {
+            c->box = make_box(lo, hi, periodic);
+            c->grid = dpd::CellGrid::make(c->box, cell_target, sub_bits);
+            c->pool = std::make_unique<dpd::WorkerPool>(workers);
+        })) {
+        delete c;
+        return nullptr;
+    }
+    return c;
+}
+
+void ref_sim_ctx_destroy(void* c) { delete static_cast<RefSimCtx*>(c); }
+
+// reorder_particles (src/cell_grid.cpp:166-198, RadixSorter src/radix_sort.cpp:16-74)
+// + local_cell_ranks + build_cell_list on the driver's arrays; *seconds covers
+// those three reference calls only (not the copies into / out of the store)
+int ref_sim_reorder(void* vc, size_t n, double* x[3], double* v[3], uint32_t* tag, uint8_t* species,
+                    uint32_t* cell_start, double* seconds) {
+    auto* c = static_cast<RefSimCtx*>(vc);
+    return guarded([&] {
+        auto& st = c->st;
+        if (st.n != n) st.resize(n);
+        for (int k = 0; k < 3; ++k) {
+            std::memcpy(st.coord[k].data(), x[k], n * 8);
+            std::memcpy(st.veloc[k].data(), v[k], n * 8);
+        }
+        std::memcpy(st.tag.data(), tag, n * 4);
+        std::memcpy(st.species.data(), species, n);
+        const auto t0 = std::chrono::steady_clock::now();
+        dpd::reorder_particles(st, c->grid, c->sorter, *c->pool);
+        const auto ranks = dpd::local_cell_ranks(st, c->grid, *c->pool);
+        dpd::build_cell_list(c->grid, ranks);
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        for (int k = 0; k < 3; ++k) {
+            std::memcpy(x[k], st.coord[k].data(), n * 8);
+            std::memcpy(v[k], st.veloc[k].data(), n * 8);
+        }
+        std::memcpy(tag, st.tag.data(), n * 4);
+        std::memcpy(species, st.species.data(), n);
+        std::memcpy(cell_start, c->grid.cell_start.data(), c->grid.cell_start.size() * 4);
     });
 }
 

@@ -135,6 +135,7 @@ SYMBOLS = {
     "dpdb_group_step_thermo": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.POINTER(Thermo)]),
     "dpdb_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "dpdb_nccl_attach": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
+    "dpdb_nccl_mock_attach": (C.c_int, [C.c_void_p, C.c_int]),
     "dpdb_dist_setup": (C.c_int, [C.c_void_p]),
     "dpdb_dist_step": (C.c_int, [C.c_void_p, C.c_int64]),
     "dpdb_dist_step_thermo": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p]),

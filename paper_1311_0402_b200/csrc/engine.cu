@@ -139,6 +139,7 @@ struct dpdb_ctx {
     // NCCL transport (one brick per process)
     void* nccl_comm = nullptr;
     int nccl_rank = -1, nccl_size = 0;
+    bool nccl_mock = false;  // attached to the in-process NCCL stand-in (tests)
     int md_peer[26]{};
     int32_t *md_dcnt{}, *md_hcnt{};      // device / pinned count exchange
     double *md_dsum{}, *md_hsum{};       // device / pinned thermo exchange
