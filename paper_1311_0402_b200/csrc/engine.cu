@@ -76,6 +76,12 @@ struct dpdb_ctx {
     // 0 = the ballot k_build (DPDB_BUILDER=ballot)
     int builder = 2;
     DevErr* err{};
+    // error polling inside long dpdb_step calls: at each rebuild the device
+    // error word is copied (async) to pinned memory; the next rebuild reads the
+    // copy if it has landed and stops the loop early on an error
+    DevErr* err_host{};
+    cudaEvent_t err_ev = nullptr;
+    bool err_pending = false;
     double *red{}, *red_out{};
     uint32_t* tmp_u32{};
     // bonds (CSR by tag; index_of_tag refreshed at every permute)
@@ -468,7 +474,8 @@ int do_permute(dpdb_ctx* ctx, bool forces) {
 
 size_t build_smem(const dpdb_ctx* ctx) {
     constexpr int P = 32 * BUILD_TILES;
-    return BUILD_WARPS * 32 * sizeof(float4) + P * 4 + ((size_t)ctx->maxn + 1) * (P + 1) * 4;
+    return BUILD_WARPS * 32 * sizeof(float4) + P * 4 + ((size_t)ctx->maxn + 1) * (P + 1) * 4 +
+           BUILD_WARPS * 32 * 4;  // + per-thread trash words
 }
 
 int launch_build(dpdb_ctx* ctx, bool joined_out);
@@ -960,11 +967,17 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         (rc = dalloc(ctx, ctx->blk_ghost, c / dpdb::FORCE_BLOCK + 1)))
         return bail(rc);
     ctx->md_list_cap = ctx->md_valid ? 8 * c : 1;  // a corner particle sits in 7 lists
+    if (cudaHostAlloc(reinterpret_cast<void**>(&ctx->err_host), sizeof(DevErr), cudaHostAllocDefault) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->err_ev, cudaEventDisableTiming) != cudaSuccess)
+        return bail(fail(ctx, DPDB_EDEVICE, "error-poll buffer"));
+    std::memset(ctx->err_host, 0, sizeof(DevErr));
     if (cudaMemset(ctx->err, 0, sizeof(DevErr)) != cudaSuccess ||
         cudaMemset(ctx->counts, 0, c * 4) != cudaSuccess ||
         // k_force_walk reads rows past their end (masked): every word must be
         // a valid particle index from the start
         cudaMemset(ctx->entries, 0, c * ctx->maxn * 4) != cudaSuccess ||
+        // and so does its phase A on the flat pair lists (prefetch past a tile's list end)
+        cudaMemset(ctx->plist, 0, (c * ctx->maxn + 512) * 4) != cudaSuccess ||
         cudaMemset(ctx->sp, 0, c) != cudaSuccess || cudaMemset(ctx->sp2, 0, c) != cudaSuccess ||
         cudaMemset(ctx->f[0], 0, c * 4) != cudaSuccess || cudaMemset(ctx->f[1], 0, c * 4) != cudaSuccess ||
         cudaMemset(ctx->f[2], 0, c * 4) != cudaSuccess)
@@ -1026,6 +1039,8 @@ int dpdb_destroy(dpdb_ctx* ctx) {
     for (size_t q = 0; q < sizeof(ptrs) / sizeof(ptrs[0]); ++q)  // each buffer once
         if (ptrs[q] && std::find(ptrs, ptrs + q, ptrs[q]) == ptrs + q) cudaFree(ptrs[q]);
     if (ctx->thermo_host) cudaFreeHost(ctx->thermo_host);
+    if (ctx->err_host) cudaFreeHost(ctx->err_host);
+    if (ctx->err_ev) cudaEventDestroy(ctx->err_ev);
     for (int k = 0; k < 3; ++k) {
         void* q[] = {ctx->x[k], ctx->v[k], ctx->x2[k], ctx->v2[k], ctx->f[k], ctx->f2[k]};
         for (void* p : q)
@@ -1791,6 +1806,27 @@ int thermo_record(dpdb_ctx* ctx, uint32_t nblocks, double* rec) {
         dpdb::k_thermo_final<<<1, 256, 0, st>>>(part, nblocks, (uint32_t)ctx->n, ctx->step, rec);
     });
 }
+// Non-blocking look at the error word: true when the copy enqueued at the
+// previous rebuild has landed and shows an error (the call then stops early;
+// check_device reports it).  Enqueues the next copy.  A row overflow or a
+// blow-up is thus caught a few rebuild periods after it happens (the host runs
+// ahead of the device by its launch queue) instead of at the end of a long
+// dpdb_step call.  Single-domain loop only: brick ranks would have to agree
+// to stop together (their collectives), so they check at the end of a call.
+bool poll_error(dpdb_ctx* ctx) {
+    if (!ctx->err_host) return false;
+    if (ctx->err_pending && cudaEventQuery(ctx->err_ev) == cudaSuccess) {
+        ctx->err_pending = false;
+        if (ctx->err_host->code) return true;
+    }
+    if (!ctx->err_pending &&
+        cudaMemcpyAsync(ctx->err_host, ctx->err, sizeof(DevErr), cudaMemcpyDeviceToHost, ctx->stream) ==
+            cudaSuccess &&
+        cudaEventRecord(ctx->err_ev, ctx->stream) == cudaSuccess)
+        ctx->err_pending = true;
+    return false;
+}
+
 int run_steps(dpdb_ctx* ctx, int64_t nsteps, double* rec = nullptr) {
     if (!ctx->have_table) return fail(ctx, DPDB_ECONFIG, "step: call dpdb_setup first");
     const bool th = rec != nullptr;
@@ -1820,6 +1856,7 @@ int run_steps(dpdb_ctx* ctx, int64_t nsteps, double* rec = nullptr) {
             ctx->step += 1;
         }
         if (rebuild) {
+            if (poll_error(ctx)) break;  // a kernel already reported an error: stop stepping
             TRY(do_sort(ctx));
             TRY(do_permute(ctx, false));
             mark(ctx, ST_SORT);

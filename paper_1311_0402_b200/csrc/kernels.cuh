@@ -686,7 +686,7 @@ __device__ __forceinline__ uint32_t build_batch_impl(const float4* slots, uint32
                                                      uint32_t j, bool valid, uint32_t ba,
                                                      uint32_t mycnt, uint32_t fl,
                                                      const BuildArgs& a, uint32_t* bufc,
-                                                     uint32_t lt, int lane) {
+                                                     uint32_t* trash, uint32_t lt, int lane) {
     const uint32_t maxn = a.maxn;
     for (uint32_t ii = 0; ii < nb; ++ii) {
         const float4 pi = slots[ii];
@@ -710,7 +710,9 @@ __device__ __forceinline__ uint32_t build_batch_impl(const float4* slots, uint32
         const uint32_t ks = maxn - 1u - ((c >> 16) + __popc(ms & lt));  // wraps on overflow
         uint32_t kp = hc ? kc : (hs ? ks : maxn);
         kp = min(kp, maxn);
-        bufc[kp * STRIDE + ii] = j;
+        // misses and overflow: each lane its own trash word (no two lanes of
+        // the CTA store to one address)
+        *(kp < maxn ? bufc + kp * STRIDE + ii : trash) = j;
         const uint32_t nw = c + __popc(mc) + ((uint32_t)__popc(ms) << 16);
         mycnt = ((uint32_t)lane == ii) ? nw : mycnt;
     }
@@ -736,6 +738,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_build(BuildArgs a) {
     uint32_t* cnt_s = reinterpret_cast<uint32_t*>(slots + WARPS * 32);
     uint32_t* buf = cnt_s + P;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t* trash = buf + (size_t)(a.maxn + 1) * STRIDE + threadIdx.x;  // one word per thread
     const uint32_t i0 = blockIdx.x * P;
     if (i0 >= a.n_local) return;
     const uint32_t iend = min(i0 + (uint32_t)P, a.n_local);
@@ -786,10 +789,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_build(BuildArgs a) {
                 const uint32_t colb = ba - i0;
                 if (fl)
                     mycnt = build_batch_impl<true, STRIDE>(slots + warp * 32, nb, pj, j, valid, ba,
-                                                           mycnt, fl, a, buf + colb, lt, lane);
+                                                           mycnt, fl, a, buf + colb, trash, lt, lane);
                 else
                     mycnt = build_batch_impl<false, STRIDE>(slots + warp * 32, nb, pj, j, valid, ba,
-                                                            mycnt, 0u, a, buf + colb, lt, lane);
+                                                            mycnt, 0u, a, buf + colb, trash, lt, lane);
             }
             if ((uint32_t)lane < nb) cnt_s[ba - i0 + lane] = mycnt;
             __syncwarp();

@@ -323,3 +323,19 @@ def test_closed_box_walls(mode):
     assert s.coord[0][0] == pytest.approx(6.0 - 0.01, abs=1e-12)
     v = [s.veloc[k][0] for k in range(3)]
     assert v == ([-2.0, 0.5, -0.25] if mode == 0 else [-2.0, -0.5, 0.25])
+
+
+def test_error_stops_a_long_step_call_early():
+    """A blow-up inside a long dpdb_step call is reported as a physics error
+    naming the particle, and the call stops a few rebuild periods after it
+    (the error word is copied and polled without a host sync at every
+    rebuild; the host runs ahead of the device by its launch queue) instead
+    of running all the remaining steps on garbage."""
+    box, obox, st = _sys.fluid((8, 8, 8), 3.0, seed=3)
+    p = dpd.PairParams.make(1, 1e30, 4.5, 1.0, 1.0, 1.0, 0.01)  # conservative force overflows
+    e = _sys.engine(box, st, params=p, run=dpd.RunConfig(rebuild_every=10))
+    e.setup()
+    with pytest.raises(dpd.DPDError) as ex:
+        e.step(5000)
+    assert ex.value.code == 2 and ("non-finite" in str(ex.value) or "blow-up" in str(ex.value))
+    assert e.current_step <= 100, e.current_step  # of 5000 requested
