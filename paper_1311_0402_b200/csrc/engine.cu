@@ -63,6 +63,7 @@ struct dpdb_ctx {
     float4 *pos4{}, *vel4{}, *vel4n{};  // n: next-step streams of the fused force pass
     int4 *posq{}, *posqn{};  // pair-force frame (PosQ) + the fused pass's next-step buffer
     uint32_t *keys{}, *keys2{}, *vals{}, *vals2{}, *hist{};
+    uint32_t* rs_work{};  // onesweep sort: tile status words, digit histograms, tile counters
     uint32_t *cell_start{}, *ostart{}, *rank_of_cell{}, *stencil{};
     uint8_t *stencil_n{}, *cell_flags{}, *stencil_code{};
     float4* cell_lo{};
@@ -370,29 +371,32 @@ int launch_integrate(dpdb_ctx* ctx, bool defer_wrap = false, bool thermo = false
 
 constexpr size_t THERMO_RING = 4096;  // records preallocated per context
 
+// onesweep LSD radix sort (kernels.cuh): one histogram pass for every digit,
+// then one binning kernel per 8-bit digit with decoupled look-back
 int radix_sort_on(dpdb_ctx* ctx, cudaStream_t st, uint32_t*& k, uint32_t*& v, uint32_t*& k2,
-                  uint32_t*& v2, uint32_t* hist, size_t n, int bits) {
+                  uint32_t*& v2, uint32_t* work, size_t n, int bits) {
     if (n == 0 || bits == 0) return 0;
-    const uint32_t tiles = (uint32_t)((n + dpdb::RS_TILE - 1) / dpdb::RS_TILE);
-    for (int shift = 0; shift < bits; shift += 8) {
-        const int width = std::min(8, bits - shift);
-        const uint32_t mask = (1u << width) - 1u;
-        uint32_t* totals = hist + (size_t)256 * tiles;
-        dpdb::k_radix_upsweep<<<tiles, dpdb::RS_THREADS, 0, st>>>(k, (uint32_t)n, shift, mask, tiles, hist);
-        dpdb::k_scan_digits<<<256, 1024, 0, st>>>(hist, tiles, totals);
-        dpdb::k_scan_totals<<<1, 256, 0, st>>>(totals);
-        dpdb::k_radix_downsweep<<<tiles, dpdb::RS_THREADS, 0, st>>>(k, v, k2, v2, (uint32_t)n, shift,
-                                                                    mask, tiles, hist, totals);
-        CKL();
-        if (ctx) ctx->launches[ST_SORT] += 4;
+    const uint32_t tiles = (uint32_t)((n + dpdb::OS_TILE - 1) / dpdb::OS_TILE);
+    const int passes = (bits + 7) / 8;
+    CK(cudaMemsetAsync(work, 0, dpdb::onesweep_work_words(n) * 4, st));
+    uint32_t* ghist = work + (size_t)4 * tiles * 256;
+    uint32_t* counters = ghist + 4 * 256;
+    dpdb::k_onesweep_hist<<<std::min<uint32_t>(tiles, 4 * 148), 256, 0, st>>>(k, (uint32_t)n, passes, ghist);
+    for (int p = 0; p < passes; ++p) {
+        const int width = std::min(8, bits - 8 * p);
+        dpdb::k_onesweep<<<tiles, dpdb::OS_THREADS, 0, st>>>(k, v, k2, v2, (uint32_t)n, 8 * p, (1u << width) - 1u,
+                                                             ghist + 256 * p, work + (size_t)p * tiles * 256,
+                                                             counters + p);
         std::swap(k, k2);
         std::swap(v, v2);
     }
+    CKL();
+    if (ctx) ctx->launches[ST_SORT] += 1 + passes;
     return 0;
 }
 
 int do_sort(dpdb_ctx* ctx) {
-    return radix_sort_on(ctx, ctx->stream, ctx->keys, ctx->vals, ctx->keys2, ctx->vals2, ctx->hist,
+    return radix_sort_on(ctx, ctx->stream, ctx->keys, ctx->vals, ctx->keys2, ctx->vals2, ctx->rs_work,
                          ctx->n, ctx->grid.key_bits());
 }
 
@@ -942,6 +946,7 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         (rc = dalloc(ctx, ctx->vel4n, c)) ||
         (rc = dalloc(ctx, ctx->keys, c)) || (rc = dalloc(ctx, ctx->keys2, c)) ||
         (rc = dalloc(ctx, ctx->vals, c)) || (rc = dalloc(ctx, ctx->vals2, c)) ||
+        (rc = dalloc(ctx, ctx->rs_work, dpdb::onesweep_work_words(c))) ||
         (rc = dalloc(ctx, ctx->hist, std::max<size_t>((size_t)256 * tiles + 256,
                                                       26 * (c / dpdb::MD_THREADS + 1) + 64))) ||
         (rc = dalloc(ctx, ctx->cell_start, (size_t)g.n_total_cells + 1)) ||
@@ -1028,7 +1033,7 @@ int dpdb_destroy(dpdb_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     md_release(ctx);
     void* ptrs[] = {ctx->tag, ctx->tag2, ctx->mol, ctx->mol2, ctx->sp, ctx->sp2, ctx->pos4,
-                    ctx->vel4, ctx->posq, ctx->posqn, ctx->vel4n, ctx->keys, ctx->keys2, ctx->vals, ctx->vals2, ctx->hist,
+                    ctx->vel4, ctx->posq, ctx->posqn, ctx->vel4n, ctx->keys, ctx->keys2, ctx->vals, ctx->vals2, ctx->hist, ctx->rs_work,
                     ctx->cell_start, ctx->ostart, ctx->rank_of_cell, ctx->stencil, ctx->stencil_n,
                     ctx->cell_flags, ctx->stencil_code, ctx->cell_lo, ctx->entries, ctx->counts, ctx->fwalk, ctx->plist, ctx->rowmeta,
                     ctx->err, ctx->red, ctx->red_out, ctx->thermo_part, ctx->thermo_part2, ctx->blk_ghost, ctx->prof_acc,
@@ -2115,13 +2120,12 @@ int dpdb_radix_sort(int device, uint32_t* keys, uint32_t* vals, size_t n, int bi
         return fail(nullptr, DPDB_ECONFIG, "radix sort: bit length must be a multiple of 4, <= 32");
     if (n == 0 || bit_length == 0) return 0;
     CK(cudaSetDevice(device));
-    const uint32_t tiles = (uint32_t)((n + dpdb::RS_TILE - 1) / dpdb::RS_TILE);
     uint32_t *k = nullptr, *v = nullptr, *k2 = nullptr, *v2 = nullptr, *h = nullptr;
     CK(cudaMalloc(&k, n * 4));
     CK(cudaMalloc(&v, n * 4));
     CK(cudaMalloc(&k2, n * 4));
     CK(cudaMalloc(&v2, n * 4));
-    CK(cudaMalloc(&h, ((size_t)256 * tiles + 256) * 4));
+    CK(cudaMalloc(&h, dpdb::onesweep_work_words(n) * 4));
     CK(cudaMemcpy(k, keys, n * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(v, vals, n * 4, cudaMemcpyHostToDevice));
     int rc = radix_sort_on(nullptr, 0, k, v, k2, v2, h, n, bit_length);

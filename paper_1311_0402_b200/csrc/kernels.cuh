@@ -369,37 +369,13 @@ __global__ void __launch_bounds__(256) k_thermo_final(const double* part, uint32
 
 // ------------------------------------------------------- radix sort
 // Stable LSD radix sort (the RadixSorter::sort contract, inc/radix_sort.hpp:11-27;
-// paper Alg. 2) with 8-bit digits: per pass an upsweep digit
-// histogram per 4096-key tile, one exclusive scan in digit-major order, and a
-// downsweep whose in-tile ranks come from warp match/ballot -- stable by
-// construction (tile order, then round, then warp, then lane).
+// paper Alg. 2) with 8-bit digits; in-tile ranks from warp
+// match/ballot -- stable by construction (tile order, then round, then warp,
+// then lane).  k_scan_digits / block_excl_scan_1024 also serve the brick
+// migration lists.
 constexpr int RS_THREADS = 256;
 constexpr int RS_ITEMS = 16;
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
-
-__global__ void __launch_bounds__(RS_THREADS) k_radix_upsweep(const uint32_t* __restrict__ keys,
-                                                              uint32_t n, int shift, uint32_t mask,
-                                                              uint32_t num_tiles,
-                                                              uint32_t* __restrict__ hist) {
-    __shared__ uint32_t h[256];
-    h[threadIdx.x] = 0;
-    const uint32_t tile = blockIdx.x;
-    const uint32_t lane = threadIdx.x & 31;
-    uint32_t d[RS_ITEMS];
-#pragma unroll
-    for (int r = 0; r < RS_ITEMS; ++r) {  // all loads in flight first
-        const uint32_t idx = tile * RS_TILE + r * RS_THREADS + threadIdx.x;
-        d[r] = idx < n ? (__ldg(keys + idx) >> shift) & mask : 256u + lane;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < RS_ITEMS; ++r) {
-        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d[r]);
-        if (d[r] < 256u && (__ffs(peers) - 1) == (int)lane) atomicAdd(&h[d[r]], (uint32_t)__popc(peers));
-    }
-    __syncthreads();
-    hist[threadIdx.x * num_tiles + tile] = h[threadIdx.x];
-}
 
 // block-wide exclusive scan helper (1024 threads)
 __device__ __forceinline__ uint32_t block_excl_scan_1024(uint32_t v, uint32_t* warp_sums,
@@ -450,91 +426,209 @@ __global__ void __launch_bounds__(1024) k_scan_digits(uint32_t* __restrict__ his
     if (threadIdx.x == 0) totals[blockIdx.x] = run;
 }
 
-// exclusive scan of the 256 digit totals -> digit bases (in place)
-__global__ void __launch_bounds__(256) k_scan_totals(uint32_t* __restrict__ totals) {
-    __shared__ uint32_t t[256];
-    t[threadIdx.x] = totals[threadIdx.x];
+// ---- onesweep LSD radix sort (single-pass digit binning with decoupled
+// look-back): one histogram kernel for every digit position, then one kernel
+// per 8-bit digit.  Each CTA takes the next 4096-key tile in launch order (a
+// tile counter, so every tile it waits on belongs to a CTA already resident),
+// ranks its keys stably, publishes its per-digit counts, looks back over the
+// earlier tiles' published counts / inclusive prefixes for its global offsets
+// (no global scan pass, no host round trip), stages the tile digit-sorted in
+// shared memory and writes it out in contiguous runs.  Stable order: tile,
+// then round, then warp, then lane -- the input index order.
+constexpr int OS_THREADS = RS_THREADS;
+constexpr int OS_ITEMS = RS_ITEMS;
+constexpr int OS_TILE = RS_TILE;
+constexpr uint32_t OS_AGG = 1u << 30, OS_INC = 2u << 30, OS_VAL = (1u << 30) - 1u;
+
+// words of sort workspace for n keys: [4][tiles][256] status, [4][256] histograms, [4] tile counters
+inline size_t onesweep_work_words(size_t n) {
+    const size_t tiles = (n + OS_TILE - 1) / OS_TILE;
+    return 4 * tiles * 256 + 4 * 256 + 32;
+}
+
+// Every thread takes 16 consecutive keys (four 16-byte loads) and adds runs
+// of equal digits at once: the input is the previous order, nearly sorted, so
+// the high digits change rarely along a run and most shared adds disappear.
+__global__ void __launch_bounds__(256) k_onesweep_hist(const uint32_t* __restrict__ keys, uint32_t n, int passes,
+                                                       uint32_t* __restrict__ ghist) {
+    __shared__ uint32_t h[4][256];
+    for (int p = 0; p < 4; ++p) h[p][threadIdx.x] = 0;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t run = 0;
-        for (int d = 0; d < 256; ++d) {
-            const uint32_t c = t[d];
-            t[d] = run;
-            run += c;
+    const uint32_t stride = gridDim.x * blockDim.x * 16u;
+    for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) * 16u; b < n; b += stride) {
+        uint32_t k[16];
+        if (b + 16 <= n) {  // the key arrays are cudaMalloc-aligned
+            const uint4* q = reinterpret_cast<const uint4*>(keys + b);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const uint4 w = __ldg(q + c);
+                k[4 * c] = w.x;
+                k[4 * c + 1] = w.y;
+                k[4 * c + 2] = w.z;
+                k[4 * c + 3] = w.w;
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < 16; ++c) k[c] = b + c < n ? __ldg(keys + b + c) : 0u;
+        }
+        const uint32_t m = min(16u, n - b);
+        for (int p = 0; p < passes; ++p) {
+            uint32_t cur = (k[0] >> (8 * p)) & 0xFFu, run = 0;
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                const uint32_t d = (k[c] >> (8 * p)) & 0xFFu;
+                if ((uint32_t)c < m && d != cur) {
+                    atomicAdd(&h[p][cur], run);
+                    cur = d;
+                    run = 0;
+                }
+                run += (uint32_t)c < m;
+            }
+            atomicAdd(&h[p][cur], run);
         }
     }
     __syncthreads();
-    totals[threadIdx.x] = t[threadIdx.x];
+    for (int p = 0; p < passes; ++p)
+        if (h[p][threadIdx.x]) atomicAdd(&ghist[p * 256 + threadIdx.x], h[p][threadIdx.x]);
+}
+
+// exclusive scan of 256 values, one per thread of a 256-thread block
+__device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t v, uint32_t* ws /*[8]*/) {
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= (uint32_t)o) incl += y;
+    }
+    if (lane == 31) ws[w] = incl;
+    __syncthreads();
+    uint32_t off = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) off += q < (int)w ? ws[q] : 0u;
+    __syncthreads();
+    return off + incl - v;
 }
 
 #ifndef DPDB_RS_BATCH
 #define DPDB_RS_BATCH 2
 #endif
-// Rounds of 256 keys are ranked RS_BATCH at a time: one barrier pair per batch
-// (the per-digit scan covers the batch's rounds in order), so the stable
-// order (tile, round, warp, lane) is unchanged.
-__global__ void __launch_bounds__(RS_THREADS) k_radix_downsweep(
+__global__ void __launch_bounds__(OS_THREADS) k_onesweep(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
-    uint32_t* __restrict__ vout, uint32_t n, int shift, uint32_t mask, uint32_t num_tiles,
-    const uint32_t* __restrict__ offs, const uint32_t* __restrict__ digit_base) {
+    uint32_t* __restrict__ vout, uint32_t n, int shift, uint32_t mask, const uint32_t* __restrict__ ghist,
+    uint32_t* status, uint32_t* tile_counter) {
     constexpr int RB = DPDB_RS_BATCH;
-    static_assert(RS_ITEMS % RB == 0, "batches must tile the rounds");
-    __shared__ uint32_t s_base[256];
-    __shared__ uint32_t s_cnt[RB][8][256];
-    __shared__ uint32_t s_pref[RB][8][256];
-    const uint32_t tile = blockIdx.x;
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t key[RS_ITEMS], val[RS_ITEMS];
-#pragma unroll
-    for (int r = 0; r < RS_ITEMS; ++r) {  // all loads in flight first
-        const uint32_t idx = tile * RS_TILE + r * RS_THREADS + threadIdx.x;
-        key[r] = idx < n ? __ldg(kin + idx) : 0u;
-        val[r] = idx < n ? __ldg(vin + idx) : 0u;
-    }
-    s_base[threadIdx.x] = offs[threadIdx.x * num_tiles + tile] + digit_base[threadIdx.x];
+    static_assert(OS_ITEMS % RB == 0, "batches must tile the rounds");
+    __shared__ uint32_t s_tile, s_ws[8];
+    __shared__ uint32_t s_run[256], s_base[256], s_lstart[256];
+    __shared__ union {
+        struct {
+            uint32_t cnt[RB][8][256], pref[RB][8][256];
+        } rk;
+        struct {
+            uint32_t k[OS_TILE], v[OS_TILE];
+        } st;
+    } u;
+    const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    if (t == 0) s_tile = atomicAdd(tile_counter, 1u);
+    s_run[t] = 0;
 #pragma unroll
     for (int rr = 0; rr < RB; ++rr)
 #pragma unroll
-        for (int w = 0; w < 8; ++w) s_cnt[rr][w][threadIdx.x] = 0;
-    __syncthreads();
-    const uint32_t lt = lanemask_lt();
+        for (int w = 0; w < 8; ++w) u.rk.cnt[rr][w][t] = 0;
+    const uint32_t gstart = block_excl_scan_256(ghist[t], s_ws);  // barriers inside
+    const uint32_t tile = s_tile;
+    const uint32_t t0 = tile * OS_TILE;
+    uint32_t key[OS_ITEMS], val[OS_ITEMS], lr[OS_ITEMS];
 #pragma unroll
-    for (int r0 = 0; r0 < RS_ITEMS; r0 += RB) {
+    for (int r = 0; r < OS_ITEMS; ++r) {  // all loads in flight first
+        const uint32_t idx = t0 + r * OS_THREADS + t;
+        key[r] = idx < n ? __ldg(kin + idx) : 0u;
+        val[r] = idx < n ? __ldg(vin + idx) : 0u;
+    }
+    const uint32_t lt = lanemask_lt();
+    // local stable ranks: per (round, warp) a match_any count per digit, then a
+    // per-digit running prefix over (round, warp) order
+#pragma unroll
+    for (int r0 = 0; r0 < OS_ITEMS; r0 += RB) {
         uint32_t d[RB], rank[RB];
 #pragma unroll
         for (int rr = 0; rr < RB; ++rr) {
             const int r = r0 + rr;
-            const uint32_t idx = tile * RS_TILE + r * RS_THREADS + threadIdx.x;
-            const bool valid = idx < n;
+            const bool valid = t0 + r * OS_THREADS + t < n;
             d[rr] = valid ? (key[r] >> shift) & mask : 256u + lane;
             const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d[rr]);
             rank[rr] = __popc(peers & lt);
-            if (valid && (__ffs(peers) - 1) == (int)lane) s_cnt[rr][warp][d[rr]] = __popc(peers);
+            if (valid && (__ffs(peers) - 1) == (int)lane) u.rk.cnt[rr][warp][d[rr]] = __popc(peers);
         }
         __syncthreads();
         {
-            uint32_t run = s_base[threadIdx.x];
+            uint32_t run = s_run[t];
 #pragma unroll
             for (int rr = 0; rr < RB; ++rr)
 #pragma unroll
                 for (int w = 0; w < 8; ++w) {
-                    const uint32_t c = s_cnt[rr][w][threadIdx.x];
-                    s_pref[rr][w][threadIdx.x] = run;
-                    s_cnt[rr][w][threadIdx.x] = 0;
+                    const uint32_t c = u.rk.cnt[rr][w][t];
+                    u.rk.pref[rr][w][t] = run;
+                    u.rk.cnt[rr][w][t] = 0;
                     run += c;
                 }
-            s_base[threadIdx.x] = run;
+            s_run[t] = run;
         }
         __syncthreads();
 #pragma unroll
-        for (int rr = 0; rr < RB; ++rr) {
-            const int r = r0 + rr;
-            if (d[rr] < 256u) {
-                const uint32_t dst = s_pref[rr][warp][d[rr]] + rank[rr];
-                kout[dst] = key[r];
-                vout[dst] = val[r];
+        for (int rr = 0; rr < RB; ++rr)
+            lr[r0 + rr] = d[rr] < 256u ? u.rk.pref[rr][warp][d[rr]] + rank[rr] : 0u;
+    }
+    // decoupled look-back, thread t = digit t
+    const uint32_t cnt = s_run[t];
+    uint32_t* my = status + (size_t)tile * 256 + t;
+    uint32_t prefix = 0;
+    if (tile == 0) {
+        __stcg(my, OS_INC | cnt);
+    } else {
+        __stcg(my, OS_AGG | cnt);
+        // windows of 8 predecessors per round trip: their status loads are
+        // independent, so a chain of published aggregates resolves 8 tiles
+        // per memory latency; a window stops at the first unpublished tile
+        // (retried) or at an inclusive prefix (done)
+        int p = (int)tile - 1;
+        bool done = false;
+        while (!done) {
+            uint32_t w[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                w[q] = p - q >= 0 ? *(const volatile uint32_t*)(status + (size_t)(p - q) * 256 + t) : OS_INC;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (done) break;
+                if ((w[q] & (OS_AGG | OS_INC)) == 0u) break;  // not published yet: retry from here
+                prefix += w[q] & OS_VAL;
+                --p;
+                done = (w[q] & OS_INC) != 0u;
             }
         }
+        __stcg(my, OS_INC | (prefix + cnt));
+    }
+    s_base[t] = gstart + prefix;
+    s_lstart[t] = block_excl_scan_256(cnt, s_ws);  // barriers inside (also fences the rank scratch)
+    __syncthreads();
+    // stage the tile digit-sorted, then write contiguous runs
+#pragma unroll
+    for (int r = 0; r < OS_ITEMS; ++r) {
+        if (t0 + r * OS_THREADS + t < n) {
+            const uint32_t pos = s_lstart[(key[r] >> shift) & mask] + lr[r];
+            u.st.k[pos] = key[r];
+            u.st.v[pos] = val[r];
+        }
+    }
+    __syncthreads();
+    const uint32_t tn = min((uint32_t)OS_TILE, n - t0);
+    for (uint32_t i = t; i < tn; i += OS_THREADS) {
+        const uint32_t k = u.st.k[i], d = (k >> shift) & mask;
+        const uint32_t dst = s_base[d] + (i - s_lstart[d]);
+        kout[dst] = k;
+        vout[dst] = u.st.v[i];
     }
 }
 
