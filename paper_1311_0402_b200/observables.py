@@ -8,6 +8,8 @@ quantities.  Pure numpy: no kernels here.
   estimate_viscosity          S:658-665  (least-squares u(z) = g rho z (d - z) / (2 mu))
   analytic_transient_profile  S:666-672  (Eq. 9)
   radial_distribution         g(r) from the pair-distance histogram
+  aggregate_shape             vesicle / micelle / bilayer classification of an
+                              amphiphile aggregate
 """
 from __future__ import annotations
 
@@ -104,3 +106,95 @@ def radial_distribution(hist, rmax, n, volume):
     shell = 4.0 / 3.0 * np.pi * (edges[1:] ** 3 - edges[:-1] ** 3)
     rho = n / volume
     return 0.5 * (edges[1:] + edges[:-1]), hist / (0.5 * n * rho * shell)
+
+
+def _unwrap_cluster(P, L, periodic, rc):
+    """Make a cluster spanning periodic images contiguous: breadth-first over
+    the contact graph (pairs within rc), each bead placed at the minimum image
+    of the neighbour it was reached from."""
+    from scipy.spatial import cKDTree
+
+    n = len(P)
+    Lp = np.where(periodic, L, 0.0)
+    Q = np.mod(P, np.where(periodic, L, np.inf)) if np.any(periodic) else P.copy()
+    tree = cKDTree(Q, boxsize=np.where(periodic, L, 0) if np.all(periodic) else None)
+    nbrs = tree.query_ball_point(Q, rc)
+    out = Q.copy()
+    seen = np.zeros(n, bool)
+    for s in range(n):
+        if seen[s]:
+            continue
+        seen[s] = True
+        stack = [s]
+        while stack:
+            i = stack.pop()
+            for j in nbrs[i]:
+                if seen[j]:
+                    continue
+                d = Q[j] - Q[i]
+                d -= Lp * np.round(d / np.where(Lp > 0, Lp, 1.0))
+                out[j] = out[i] + d
+                seen[j] = True
+                stack.append(j)
+    return out
+
+
+@dataclass
+class AggregateShape:
+    """Shape of one aggregate (e.g. the tail beads of the largest cluster)."""
+    n: int
+    radius_of_gyration: float
+    asphericity: float      # 0 sphere .. 1 rod (gyration-tensor eigenvalues)
+    hollowness: float       # bead density within 0.4 Rg of the centre relative to a
+                            # uniform solid ball of the same Rg (1 solid .. 0 hollow)
+    closure: float          # fraction of 162 directions from the centre that hit the aggregate
+    kind: str               # "vesicle" | "micelle" | "bilayer" | "irregular"
+
+
+def aggregate_shape(coords, box, rc: float = 1.0) -> AggregateShape:
+    """Vesicle observable ("spontaneous vesicle formation"; S:692
+    cluster trace).  coords: (n, 3) bead positions of ONE aggregate (periodic
+    images are joined through its contact graph).  A vesicle is a closed,
+    hollow, near-spherical shell: hollowness < 0.25 (the centre is empty
+    where a micelle or a solid ball is full), closure >= 0.9 (beads seen in
+    almost every direction from the centre, unlike a bilayer patch or an
+    open cup) and asphericity < 0.2; a micelle is closed, near-spherical and
+    solid; a bilayer is flat (its smallest gyration eigenvalue < 5% of the
+    largest)."""
+    P = np.asarray(coords, np.float64).reshape(-1, 3)
+    n = len(P)
+    if n < 8:
+        return AggregateShape(n, 0.0, 0.0, 1.0, 0.0, "irregular")
+    L = np.array([box.length(k) for k in range(3)])
+    per = np.array(box.periodic, bool)
+    X = _unwrap_cluster(P - np.array(box.lo), L, per, rc)
+    c = X.mean(0)
+    D = X - c
+    G = D.T @ D / n
+    ev = np.sort(np.linalg.eigvalsh(G))
+    rg = float(np.sqrt(ev.sum()))
+    tr = ev.sum()
+    asph = float(((ev[2] - ev[1]) ** 2 + (ev[2] - ev[0]) ** 2 + (ev[1] - ev[0]) ** 2) / (2 * tr * tr))
+    r = np.linalg.norm(D, axis=1)
+    # uniform solid ball with this Rg: R = Rg sqrt(5/3); fraction within a of the centre = (a/R)^3
+    R = rg * np.sqrt(5.0 / 3.0)
+    a = 0.4 * rg
+    hollow = float((r < a).mean() / max((a / R) ** 3, 1e-12))
+    # directions: a 162-vertex geodesic sphere (Fibonacci lattice)
+    k = np.arange(162) + 0.5
+    th = np.arccos(1 - 2 * k / 162)
+    ph = np.pi * (1 + 5 ** 0.5) * k
+    U = np.stack([np.sin(th) * np.cos(ph), np.sin(th) * np.sin(ph), np.cos(th)], 1)
+    Dn = D / np.maximum(r, 1e-12)[:, None]
+    cosmax = np.cos(np.deg2rad(12.0))
+    closure = float(((Dn @ U.T) > cosmax).any(0).mean())
+    flat = ev[0] < 0.05 * ev[2]
+    if hollow < 0.25 and closure >= 0.9 and asph < 0.2:
+        kind = "vesicle"
+    elif flat:
+        kind = "bilayer"
+    elif closure >= 0.9 and asph < 0.2:
+        kind = "micelle"
+    else:
+        kind = "irregular"
+    return AggregateShape(n, rg, asph, hollow, closure, kind)

@@ -245,12 +245,18 @@ def largest_cluster(coords, species, molecule, box: SimBox, members, rc: float =
     """S:692 cluster analysis: union-find over the beads of the `members`
     species closer than rc (minimum image on periodic axes); returns (beads,
     molecules) of the largest cluster."""
+    beads, mols, _ = cluster_members(coords, species, molecule, box, members, rc)
+    return beads, mols
+
+
+def cluster_members(coords, species, molecule, box: SimBox, members, rc: float = 1.0):
+    """largest_cluster, plus the particle indices of that cluster's beads."""
     from scipy.spatial import cKDTree
 
     sel = np.isin(species, list(members))
     idx = np.flatnonzero(sel)
     if not len(idx):
-        return 0, 0
+        return 0, 0, idx
     P = np.stack([np.asarray(c)[idx] - box.lo[k] for k, c in enumerate(coords)], 1)
     L = np.array([box.length(k) for k in range(3)])
     P = np.mod(P, L)
@@ -269,10 +275,11 @@ def largest_cluster(coords, species, molecule, box: SimBox, members, rc: float =
         if ri != rj:
             parent[max(ri, rj)] = min(ri, rj)
     roots = np.array([find(i) for i in range(len(idx))])
-    best = (0, 0)
+    best, best_idx = (0, 0), idx[:0]
     mol = np.asarray(molecule)[idx]
     for r_ in np.unique(roots):
         m = roots == r_
         cand = (int(m.sum()), len(np.unique(mol[m])))
-        best = max(best, cand, key=lambda t: (t[1], t[0]))
-    return best
+        if (cand[1], cand[0]) > (best[1], best[0]):
+            best, best_idx = cand, idx[m]
+    return best[0], best[1], best_idx
