@@ -1121,6 +1121,10 @@ constexpr int RB_THREADS = DPDB_RB_THREADS;  // lanes per CTA (RB_BLOCK / RB_THR
 constexpr int RB_SLOTS = 29;     // 27 stencil cells + one split by the cut-out + a trash slot
 constexpr size_t RB_SMEM = (size_t)RB_SLOTS * RB_THREADS * 6;
 constexpr uint32_t RB_NONE = 0xFFFFFFFFu;
+#ifndef DPDB_RB_AHEAD
+#define DPDB_RB_AHEAD 2
+#endif
+constexpr int RB_AHEAD = DPDB_RB_AHEAD;  // walk lookahead (A/B: 2 vs 4 position loads in flight per lane)
 
 // Rows whose front count + cut-out length could exceed max_neighbors: the
 // exact number of in-block j < i within r_c + skin (the row's back entries),
@@ -1272,8 +1276,6 @@ __global__ void __launch_bounds__(RB_THREADS, 1024 / RB_THREADS) k_build_range(B
             cj = rs[0][t];
             ce = cj + rl[0][t];
         }
-        uint32_t j0, j1;
-        bool v0, v1;
         auto adv = [&](uint32_t& j, bool& v) {
             v = cj < ce;
             if (!v && cs + 1 < nr) {
@@ -1285,9 +1287,14 @@ __global__ void __launch_bounds__(RB_THREADS, 1024 / RB_THREADS) k_build_range(B
             j = v ? cj : i;
             cj += v;
         };
-        adv(j0, v0);
-        adv(j1, v1);
-        float4 p0 = __ldg(a.pos4 + j0), p1 = __ldg(a.pos4 + j1);
+        // RB_AHEAD candidates in flight per lane (cursor RB_AHEAD ahead of the test)
+        uint32_t jq[RB_AHEAD];
+        bool vq[RB_AHEAD];
+        float4 pq[RB_AHEAD];
+#pragma unroll
+        for (int q = 0; q < RB_AHEAD; ++q) adv(jq[q], vq[q]);
+#pragma unroll
+        for (int q = 0; q < RB_AHEAD; ++q) pq[q] = __ldg(a.pos4 + jq[q]);
         uint32_t* rowp = a.entries + (size_t)(i & ~31u) * maxn + (i & 31u);
         uint32_t* wp = rowp;
         const int wstep = 32 - 31 * (int)maxn;  // entry 32q+31 -> 32(q+1)
@@ -1337,13 +1344,13 @@ __global__ void __launch_bounds__(RB_THREADS, 1024 / RB_THREADS) k_build_range(B
                 nc += hit && core;
                 nsk += hit && !core;
             };
-            while (__any_sync(0xFFFFFFFFu, v0)) {
-                test(j0, p0, v0);
-                adv(j0, v0);
-                p0 = __ldg(a.pos4 + j0);
-                test(j1, p1, v1);
-                adv(j1, v1);
-                p1 = __ldg(a.pos4 + j1);
+            while (__any_sync(0xFFFFFFFFu, vq[0])) {
+#pragma unroll
+                for (int q = 0; q < RB_AHEAD; ++q) {
+                    test(jq[q], pq[q], vq[q]);
+                    adv(jq[q], vq[q]);
+                    pq[q] = __ldg(a.pos4 + jq[q]);
+                }
             }
         };
         if (anywrap)
