@@ -1811,16 +1811,19 @@ int thermo_record(dpdb_ctx* ctx, uint32_t nblocks, double* rec) {
         dpdb::k_thermo_final<<<1, 256, 0, st>>>(part, nblocks, (uint32_t)ctx->n, ctx->step, rec);
     });
 }
-// Non-blocking look at the error word: true when the copy enqueued at the
-// previous rebuild has landed and shows an error (the call then stops early;
-// check_device reports it).  Enqueues the next copy.  A row overflow or a
-// blow-up is thus caught a few rebuild periods after it happens (the host runs
-// ahead of the device by its launch queue) instead of at the end of a long
+// Look at the error word: true when the copy enqueued at the previous
+// rebuild shows an error (the call then stops early; check_device reports
+// it).  Enqueues the next copy.  A row overflow or a blow-up is thus caught
+// within two rebuild periods of happening instead of at the end of a long
 // dpdb_step call.  Single-domain loop only: brick ranks would have to agree
 // to stop together (their collectives), so they check at the end of a call.
 bool poll_error(dpdb_ctx* ctx) {
     if (!ctx->err_host) return false;
-    if (ctx->err_pending && cudaEventQuery(ctx->err_ev) == cudaSuccess) {
+    // wait for the previous rebuild's copy: the host then runs at most one
+    // rebuild period ahead of the device (that period's launches keep the
+    // device fed meanwhile), so a small system cannot queue thousands of
+    // steps past an error
+    if (ctx->err_pending && cudaEventSynchronize(ctx->err_ev) == cudaSuccess) {
         ctx->err_pending = false;
         if (ctx->err_host->code) return true;
     }
