@@ -1276,28 +1276,27 @@ __global__ void __launch_bounds__(RB_THREADS, 1024 / RB_THREADS) k_build_range(B
             cj = rs[0][t];
             ce = cj + rl[0][t];
         }
-        auto adv = [&](uint32_t& j, bool& v) {
+        // (flags as 0/1 words: bool arrays cost byte packing on every step)
+        auto adv = [&](uint32_t& j, uint32_t& v) {
             v = cj < ce;
             if (!v && cs + 1 < nr) {
                 ++cs;
                 cj = rs[cs][t];
                 ce = cj + rl[cs][t];
-                v = true;
+                v = 1u;
             }
             j = v ? cj : i;
             cj += v;
         };
         // RB_AHEAD candidates in flight per lane (cursor RB_AHEAD ahead of the test)
         uint32_t jq[RB_AHEAD];
-        bool vq[RB_AHEAD];
+        uint32_t vq[RB_AHEAD];
         float4 pq[RB_AHEAD];
 #pragma unroll
         for (int q = 0; q < RB_AHEAD; ++q) adv(jq[q], vq[q]);
 #pragma unroll
         for (int q = 0; q < RB_AHEAD; ++q) pq[q] = __ldg(a.pos4 + jq[q]);
         uint32_t* rowp = a.entries + (size_t)(i & ~31u) * maxn + (i & 31u);
-        uint32_t* wp = rowp;
-        const int wstep = 32 - 31 * (int)maxn;  // entry 32q+31 -> 32(q+1)
         uint32_t kf = 0, kb = 0, nc = 0, nsk = 0;
         const float cut_s = a.cut_s, cut_c = a.cut_c;
         // branch-free min image (min_image_f semantics): axes without wrap get
@@ -1314,7 +1313,7 @@ __global__ void __launch_bounds__(RB_THREADS, 1024 / RB_THREADS) k_build_range(B
         // issue no minimum-image instructions at all
         auto walk = [&](auto wrapc) {
             constexpr bool WRAPW = decltype(wrapc)::value;
-            auto test = [&](uint32_t j, float4 pj, bool v) {
+            auto test = [&](uint32_t j, float4 pj, uint32_t v) {
                 float dx = __fsub_rn(pi.x, pj.x);
                 float dy = __fsub_rn(pi.y, pj.y);
                 float dz = __fsub_rn(pi.z, pj.z);
@@ -1329,11 +1328,12 @@ __global__ void __launch_bounds__(RB_THREADS, 1024 / RB_THREADS) k_build_range(B
                 const bool core = d2 <= cut_c;
                 if (GH && hit && j >= a.n_local) ghost_seen = 1u;  // same value from every writer
                 if (WALK) {
-                    // predicated store into the tile-transposed scratch rows (no branch)
+                    // predicated store into the tile-transposed scratch rows (no
+                    // branch); the slot of entry kf from kf itself (raw_index)
+                    const uint32_t* wp = rowp + ((kf & 31u) * maxn + (kf & ~31u));
                     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.global.u32 [%0], %1;\n\t}"
                                  ::"l"(wp), "r"(core ? j : (j | 0x80000000u)),
                                  "r"((uint32_t)(hit && kf < maxn)));
-                    wp += hit ? (((kf & 31u) == 31u) ? wstep : (int)maxn) : 0;
                     kf += hit;
                 } else {
                     const uint32_t k = core ? kf : maxn - 1u - kb;
