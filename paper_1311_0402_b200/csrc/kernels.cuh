@@ -1276,24 +1276,26 @@ __global__ void __launch_bounds__(RB_THREADS, 1024 / RB_THREADS) k_build_range(B
             cj = rs[0][t];
             ce = cj + rl[0][t];
         }
-        // (flags as 0/1 words: bool arrays cost byte packing on every step)
-        auto adv = [&](uint32_t& j, uint32_t& v) {
-            v = cj < ce;
-            if (!v && cs + 1 < nr) {
+        // The next candidate, or i itself once the lane's ranges are exhausted
+        // (the ranges never hold i: the sentinel needs no separate flag, which
+        // the compiler would carry as a byte or a 0/1 word across the loop).
+        // Ranges are non-empty, so a switch always yields a candidate.
+        auto adv = [&]() -> uint32_t {
+            if (cj >= ce && cs + 1 < nr) {
                 ++cs;
                 cj = rs[cs][t];
                 ce = cj + rl[cs][t];
-                v = 1u;
             }
-            j = v ? cj : i;
+            const bool v = cj < ce;
+            const uint32_t j = v ? cj : i;
             cj += v;
+            return j;
         };
         // RB_AHEAD candidates in flight per lane (cursor RB_AHEAD ahead of the test)
         uint32_t jq[RB_AHEAD];
-        uint32_t vq[RB_AHEAD];
         float4 pq[RB_AHEAD];
 #pragma unroll
-        for (int q = 0; q < RB_AHEAD; ++q) adv(jq[q], vq[q]);
+        for (int q = 0; q < RB_AHEAD; ++q) jq[q] = adv();
 #pragma unroll
         for (int q = 0; q < RB_AHEAD; ++q) pq[q] = __ldg(a.pos4 + jq[q]);
         uint32_t* rowp = a.entries + (size_t)(i & ~31u) * maxn + (i & 31u);
@@ -1313,7 +1315,7 @@ __global__ void __launch_bounds__(RB_THREADS, 1024 / RB_THREADS) k_build_range(B
         // issue no minimum-image instructions at all
         auto walk = [&](auto wrapc) {
             constexpr bool WRAPW = decltype(wrapc)::value;
-            auto test = [&](uint32_t j, float4 pj, uint32_t v) {
+            auto test = [&](uint32_t j, float4 pj) {
                 float dx = __fsub_rn(pi.x, pj.x);
                 float dy = __fsub_rn(pi.y, pj.y);
                 float dz = __fsub_rn(pi.z, pj.z);
@@ -1324,7 +1326,7 @@ __global__ void __launch_bounds__(RB_THREADS, 1024 / RB_THREADS) k_build_range(B
                 }
                 const float d2 =
                     __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
-                const bool hit = v && d2 <= cut_s;
+                const bool hit = j != i && d2 <= cut_s;
                 const bool core = d2 <= cut_c;
                 if (GH && hit && j >= a.n_local) ghost_seen = 1u;  // same value from every writer
                 if (WALK) {
@@ -1344,11 +1346,11 @@ __global__ void __launch_bounds__(RB_THREADS, 1024 / RB_THREADS) k_build_range(B
                 nc += hit && core;
                 nsk += hit && !core;
             };
-            while (__any_sync(0xFFFFFFFFu, vq[0])) {
+            while (__any_sync(0xFFFFFFFFu, jq[0] != i)) {
 #pragma unroll
                 for (int q = 0; q < RB_AHEAD; ++q) {
-                    test(jq[q], pq[q], vq[q]);
-                    adv(jq[q], vq[q]);
+                    test(jq[q], pq[q]);
+                    jq[q] = adv();
                     pq[q] = __ldg(a.pos4 + jq[q]);
                 }
             }
