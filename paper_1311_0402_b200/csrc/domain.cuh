@@ -253,6 +253,63 @@ __device__ __forceinline__ uint32_t ghost_key_of(const DevGrid& g, const double 
     return (rank << (3 * g.sub_bits)) | sub;
 }
 
+// Ghost update as one put (Alg. 6's "border determination + put"):
+// the sender reads each send-list particle's fp64 state and writes it, with
+// the periodic image shift of its direction, straight into the receiving
+// brick's ghost slot -- x, v and the receiver-frame fp32 streams (pos4, posq,
+// vel4 + signature), the same arithmetic as k_pack + k_unpack<false> -- with
+// plain stores through the receiver's pointers (device memory of another
+// brick on this GPU, or of a peer GPU over NVLink with peer access on).  No
+// record buffer, no copy, no unpack launch.
+struct PutDir {  // the receiver in one direction of the sender
+    double* x[3];
+    double* v[3];
+    const uint32_t* tag;
+    const uint8_t* sp;
+    const uint32_t* slot_of;  // receiver's receive index -> ghost slot (fixed at the rebuild)
+    float4* pos4;
+    int4* posq;
+    float4* vel4;
+    PosQ pq;
+    double centre[3];
+    double shift[3];  // sender-side periodic image shift of this direction
+    uint32_t rbase;   // receiver's receive index of this direction's first record
+    int multi;
+};
+
+struct PutArgs {
+    const double* x[3];
+    const double* v[3];
+    const uint32_t* lists;  // sender's concatenated send lists
+    uint32_t off[27];       // list offsets per direction
+    uint32_t total;
+    PutDir dir[26];
+};
+
+__global__ void __launch_bounds__(256) k_put(const __grid_constant__ PutArgs a) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= a.total) return;
+    const int d = find_dir(a.off, s);
+    const PutDir& P = a.dir[d];
+    const uint32_t i = a.lists[s];
+    const uint32_t g = P.slot_of[P.rbase + (s - a.off[d])];
+    double x[3], v[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        x[k] = __dadd_rn(a.x[k][i], P.shift[k]);
+        v[k] = a.v[k][i];
+        P.x[k][g] = x[k];
+        P.v[k][g] = v[k];
+    }
+    const uint32_t tag = P.tag[g];
+    const uint32_t tw = P.multi ? (tag | ((uint32_t)P.sp[g] << 28)) : tag;
+    const uint32_t sig = make_signature(tag, v[0], v[1], v[2]);
+    P.pos4[g] = make_float4((float)(x[0] - P.centre[0]), (float)(x[1] - P.centre[1]),
+                            (float)(x[2] - P.centre[2]), __uint_as_float(tw));
+    P.posq[g] = posq_of(P.pq, x[0], x[1], x[2], tw);
+    P.vel4[g] = make_float4((float)v[0], (float)v[1], (float)v[2], __uint_as_float(sig));
+}
+
 template <bool FULL>
 __global__ void k_unpack(UnpackArgs a, const void* in) {
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;

@@ -191,6 +191,30 @@ def test_overlapped_halo_update_is_bitwise_blocking(monkeypatch, L, dims):
         assert np.array_equal(u, w)
 
 
+@pytest.mark.parametrize("L,dims", [((40, 24, 24), (2, 1, 1)), ((36, 36, 36), (2, 2, 2)),
+                                    ((14, 13, 12), (3, 2, 1)), ((24, 24, 24), (2, 2, 1))])
+def test_put_halo_update_is_bitwise_pack_copy_unpack(monkeypatch, L, dims):
+    """The ghost update as one k_put per sender (straight into the receivers'
+    ghost slots, Alg. 6) equals the pack -> peer copy -> unpack update bit
+    for bit: forces, positions, velocities, thermo records, across rebuilds
+    (the receiver slots and send lists change) and fused / unfused steps."""
+    box, obox, st = _sys.fluid(L, 3.0, seed=43)
+    run = dpd.RunConfig(rebuild_every=4)
+    out = []
+    for put in ("1", "0"):
+        monkeypatch.setenv("DPDB_PUT", put)
+        g = group(box, st, run, dims)
+        rec = g.step_thermo(11)
+        out.append((g.download(), rec))
+        g.close()
+    (a, ra), (b, rb) = out
+    assert np.array_equal(a.tag, b.tag)
+    for u, w in zip(a.coord + a.veloc + a.force, b.coord + b.veloc + b.force):
+        assert np.array_equal(u, w)
+    for k in ra:
+        assert np.array_equal(ra[k], rb[k])
+
+
 @pytest.mark.parametrize("dims", [(2, 1, 1), (2, 2, 2)])
 def test_group_step_thermo_records(dims):
     """dpdb_group_step_thermo: per-step thermo of a brick run reduced on the
