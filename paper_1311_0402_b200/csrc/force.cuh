@@ -442,7 +442,17 @@ constexpr bool FW_UNCOND = DPDB_FW_UNCOND;
 #define DPDB_FW_PREFETCH 0
 #endif
 constexpr bool FW_PREFETCH = DPDB_FW_PREFETCH;  // A/B switch: L1 prefetch of vel4[j] in phase A
-constexpr int FW_Q = 160;  // < 32 leftovers + 4 x 32 hits per group
+// Interleaved drain: the queue is drained FW_IL batches at a time, lane l of
+// batch b taking entry l * FW_IL + b.  Queued pairs are in row order (a row's
+// ~8 pairs contiguous), so a plain batch of 32 consecutive pairs has ~8 lanes
+// per owner row and its i-side shared atomics serialise on the same address
+// (~8 L1 wavefronts each: the shared atomics were 31% of the L1 data pipe,
+// which ran at 91%); interleaving spreads each batch over FW_IL x as many rows.
+#ifndef DPDB_FW_IL
+#define DPDB_FW_IL 2
+#endif
+constexpr int FW_IL = DPDB_FW_IL;
+constexpr int FW_Q = 32 * FW_IL + 128;  // < 32 FW_IL leftovers + 4 x 32 hits per group
 
 template <bool GENERAL, bool BODY, int MAXN, int FUSE>
 __global__ void __launch_bounds__(FORCE_WARPS * 32, GENERAL ? 32 / FORCE_WARPS : FW_MINB)
@@ -486,9 +496,9 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, GENERAL ? 32 / FORCE_WARPS :
         __syncwarp();
         uint32_t qtail = 0;
 
-        auto process = [&](uint32_t h, uint32_t cnt) {
-            if ((uint32_t)lane < cnt) {
-                const uint32_t jw = q_j[warp][h + lane];
+        auto process = [&](uint32_t e, bool valid) {  // queue entry e on this lane
+            if (valid) {
+                const uint32_t jw = q_j[warp][e];
                 const uint32_t o = (jw >> 26) & 31u, j = jw & 0x03FFFFFFu;
                 const int4 po = own_p[warp][o];
                 const float4 vo = own_v[warp][o];
@@ -568,19 +578,30 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, GENERAL ? 32 / FORCE_WARPS :
                     asm volatile("prefetch.global.L1 [%0];" ::"l"(vb + ((size_t)(cur[k] & 0x03FFFFFFu) << 4)));
                 qtail += __popc(bal);
             }
-            // drain whole batches, then move the (< 32) leftovers to the front
-            if (qtail >= 32u) {
+            // drain FW_IL interleaved batches, then move the (< 32 FW_IL)
+            // leftovers to the front
+            if (qtail >= 32u * FW_IL) {
                 __syncwarp();
                 uint32_t h = 0;
                 do {
-                    process(h, 32u);
-                    h += 32u;
-                } while (qtail - h >= 32u);
+#pragma unroll
+                    for (int b = 0; b < FW_IL; ++b) process(h + (uint32_t)lane * FW_IL + b, true);
+                    h += 32u * FW_IL;
+                } while (qtail - h >= 32u * FW_IL);
                 __syncwarp();
                 const uint32_t left = qtail - h;
-                const uint32_t mv = (uint32_t)lane < left ? qw[h + lane] : 0u;
+                uint32_t mv[FW_IL];
+#pragma unroll
+                for (int b = 0; b < FW_IL; ++b) {
+                    const uint32_t e = (uint32_t)lane + 32u * b;
+                    mv[b] = e < left ? qw[h + e] : 0u;
+                }
                 __syncwarp();
-                if ((uint32_t)lane < left) qw[lane] = mv;
+#pragma unroll
+                for (int b = 0; b < FW_IL; ++b) {
+                    const uint32_t e = (uint32_t)lane + 32u * b;
+                    if (e < left) qw[e] = mv[b];
+                }
                 __syncwarp();
                 qtail = left;
             }
@@ -595,7 +616,13 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, GENERAL ? 32 / FORCE_WARPS :
             group(c0 + 128, eb, ea);
         }
         __syncwarp();
-        if (qtail > 0) process(0u, qtail);
+        if (qtail > 0) {  // the rest, interleaved the same way
+            const uint32_t nb = (qtail + 31u) >> 5;
+            for (uint32_t b = 0; b < nb; ++b) {
+                const uint32_t e = (uint32_t)lane * nb + b;
+                process(e, e < qtail);
+            }
+        }
         __syncwarp();
     }
     if (coincident) raise_err(a.err, DPDB_EPHYSICS, EW_COINCIDENT, bad_tag, 0u);
