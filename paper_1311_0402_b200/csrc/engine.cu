@@ -104,6 +104,9 @@ struct dpdb_ctx {
     bool has_mol = false, have_sorted = false, have_table = false, tiled = true, joined = false;
     bool multi = false;  // n_species > 1: species packed into pos4.w bits 28-31
     bool no_fuse = false;  // DPDB_FUSE=0: keep the Verlet pass a separate kernel (A/B)
+    // range builder: flat pair lists grouped by partner line; DPDB_BUCKET=0
+    // keeps the row order (A/B)
+    bool bucket_lists = true;
     uint32_t num_sms = 148;   // multiprocessors of the device
     // per-step thermo (dpdb_step_thermo): block partials of the phase-2 pass
     // and the records, written by the device straight into mapped pinned memory
@@ -525,6 +528,7 @@ int launch_build(dpdb_ctx* ctx, bool joined_out) {
     a.rowmeta = ctx->rowmeta;
     a.plist = ctx->plist;
     a.force_block = dpdb::FORCE_BLOCK;
+    a.bucket = ctx->bucket_lists ? 1 : 0;
     a.err = ctx->err;
     a.n_local = (uint32_t)ctx->n;
     a.maxn = ctx->maxn;
@@ -863,6 +867,7 @@ int dpdb_create(int device, const dpdb_box* box, const dpdb_params* params, cons
         ctx->builder = !std::strcmp(b, "ballot") ? 0 : !std::strcmp(b, "lane") ? 1 : 2;
     ctx->multi = params->n_species > 1;
     if (const char* f = std::getenv("DPDB_FUSE")) ctx->no_fuse = std::strcmp(f, "0") == 0;
+    if (const char* f = std::getenv("DPDB_BUCKET")) ctx->bucket_lists = std::strcmp(f, "0") != 0;
     {
         int sms = 0;
         if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0)

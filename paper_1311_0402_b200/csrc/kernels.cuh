@@ -759,6 +759,7 @@ struct BuildArgs {
     uint8_t* blk_ghost;           // per force block: any row with a ghost partner (j >= n_local)
     float csz[3];                 // cell side per axis (fp32)
     float cut_cull;               // (r_c + skin + margin)^2
+    int bucket;                   // k_build_range walk layout: flat lists grouped by partner line
 };
 
 // fp32 minimum image, src/core.cpp:129-139 semantics with L, L/2 in fp32
@@ -1361,7 +1362,86 @@ __global__ void __launch_bounds__(RB_THREADS, 1024 / RB_THREADS) k_build_range(B
             walk(std::false_type{});
         cnt[pass] = min(nc, 0xFFFFu) | (min(nsk, 0xFFFFu) << 16);  // saturate: >= 65535 overflows maxn anyway
         kfs[pass] = kf;
-        if (WALK) {
+        if (WALK && a.bucket) {
+            // The tile's flat pair list for the force kernel, grouped by the
+            // partner's cache line: the 32 rows of a tile are neighbours and
+            // share most candidates (C3: ~577 items, ~160 distinct partners in
+            // ~47 lines of 8 particles), so with the items of a line side by
+            // side a 32-lane gather of the force kernel touches a few lines
+            // instead of ~20 (row order) and its pair batches hold distinct
+            // owner rows.  A counting sort on a 4-bit hash of the line: each
+            // lane (row) counts its own items in its column of a [bucket][lane]
+            // u16 histogram (this warp's share of rl), a scan turns the counts
+            // into offsets in (bucket, row) order, the items are placed in this
+            // warp's share of rs (both free after the walk) and written out
+            // coalesced.  No atomics, deterministic; order = bucket, row,
+            // ascending j.  Tiles longer than the staging keep the row order.
+            const uint32_t lane = t & 31u, wbase = t & ~31u;
+            const uint32_t kfc = min(kf, maxn);
+            uint32_t tot = kfc;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) tot += __shfl_xor_sync(0xFFFFFFFFu, tot, d);
+            constexpr uint32_t STG = RB_SLOTS * 32;  // staging words per warp
+            uint32_t* tl = a.plist + (size_t)(i & ~31u) * maxn;
+            const uint32_t rowbits = lane << 26;
+            auto bucket_of = [](uint32_t e) { return (((e & 0x03FFFFFFu) >> 3) * 0x9E3779B1u) >> 28; };
+            auto hist = [&](uint32_t h) -> uint16_t& { return rl[h >> 5][wbase + (h & 31u)]; };  // h = b*32 + lane
+            __syncwarp();
+            if (tot <= STG) {
+#pragma unroll
+                for (uint32_t b = 0; b < 16; ++b) hist(b * 32u + lane) = 0;
+                for (uint32_t m = 0; m < kfc; ++m) {
+                    uint16_t& h = hist(bucket_of(rowp[(m & 31u) * maxn + (m & ~31u)]) * 32u + lane);
+                    h = (uint16_t)(h + 1u);
+                }
+                __syncwarp();
+                // exclusive offsets in (bucket, lane) order: lanes 2b, 2b+1
+                // scan the two halves of bucket b's 32 counters
+                {
+                    const uint32_t b = lane >> 1, l0 = (lane & 1u) * 16u;
+                    uint32_t c[16], run = 0;
+#pragma unroll
+                    for (uint32_t l = 0; l < 16; ++l) {
+                        c[l] = hist(b * 32u + l0 + l);
+                        run += c[l];
+                    }
+                    uint32_t incl = run;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+                        if (lane >= (uint32_t)d) incl += y;
+                    }
+                    uint32_t o = incl - run;
+                    __syncwarp();
+#pragma unroll
+                    for (uint32_t l = 0; l < 16; ++l) {
+                        hist(b * 32u + l0 + l) = (uint16_t)o;
+                        o += c[l];
+                    }
+                }
+                __syncwarp();
+                for (uint32_t m = 0; m < kfc; ++m) {
+                    const uint32_t e = rowp[(m & 31u) * maxn + (m & ~31u)];
+                    uint16_t& h = hist(bucket_of(e) * 32u + lane);
+                    const uint32_t q = h;
+                    rs[q >> 5][wbase + (q & 31u)] = (e & 0x83FFFFFFu) | rowbits;
+                    h = (uint16_t)(q + 1u);
+                }
+                __syncwarp();
+                for (uint32_t q = lane; q < tot; q += 32) tl[q] = rs[q >> 5][wbase + (q & 31u)];
+                __syncwarp();
+            } else {  // row order, straight from the rows
+                uint32_t off = kfc;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, off, d);
+                    if (lane >= (uint32_t)d) off += y;
+                }
+                off -= kfc;
+                for (uint32_t m = 0; m < kfc; ++m)
+                    tl[off + m] = (rowp[(m & 31u) * maxn + (m & ~31u)] & 0x83FFFFFFu) | rowbits;
+            }
+        } else if (WALK) {
             // The tile's flat pair list for the force kernel: the warp's rows
             // back-to-back in row order (exclusive warp scan of the row
             // lengths), each item j | row << 26 | skin << 31.  The rows just
