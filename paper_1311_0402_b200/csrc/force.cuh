@@ -442,14 +442,14 @@ constexpr bool FW_UNCOND = DPDB_FW_UNCOND;
 #define DPDB_FW_PREFETCH 0
 #endif
 constexpr bool FW_PREFETCH = DPDB_FW_PREFETCH;  // A/B switch: L1 prefetch of vel4[j] in phase A
-// Interleaved drain: the queue is drained FW_IL batches at a time, lane l of
-// batch b taking entry l * FW_IL + b.  Queued pairs are in row order (a row's
-// ~8 pairs contiguous), so a plain batch of 32 consecutive pairs has ~8 lanes
-// per owner row and its i-side shared atomics serialise on the same address
-// (~8 L1 wavefronts each: the shared atomics were 31% of the L1 data pipe,
-// which ran at 91%); interleaving spreads each batch over FW_IL x as many rows.
+// Interleaved drain (A/B knob): the queue is drained FW_IL batches at a time,
+// lane l of batch b taking entry l * FW_IL + b.  With row-ordered flat lists a
+// plain batch of 32 consecutive pairs has ~8 lanes per owner row and its
+// i-side shared atomics serialise on one address (IL 2 was 1% faster there);
+// the builder's line-grouped lists already mix the rows of a batch, and IL 1
+// is faster (0.442 vs 0.448 ms).
 #ifndef DPDB_FW_IL
-#define DPDB_FW_IL 2
+#define DPDB_FW_IL 1
 #endif
 constexpr int FW_IL = DPDB_FW_IL;
 constexpr int FW_Q = 32 * FW_IL + 128;  // < 32 FW_IL leftovers + 4 x 32 hits per group
