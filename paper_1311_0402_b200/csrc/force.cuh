@@ -87,10 +87,13 @@ __device__ __forceinline__ float lg2_ftz(float x) {
 // |xi - xi_ref| < 4e-6 over the whole word range (test_gpu_rng).
 __device__ __forceinline__ float gaussian_hot(uint32_t ua, uint32_t ub) {
     ua = max(ua, 1u);
-    const float la = lg2_ftz(__uint2float_rn(ua) * 0x1p-32f);     // log2 u, u < 1
-    const float t = __uint2float_rn(0u - ua) * 0x1p-32f;          // 1 - u (exact near 1)
-    const float lb = t * fmaf(t, fmaf(t, 0.333333333f, 0.5f), 1.0f);  // -ln u near 1
-    const float m2 = ua >= 0xFF000000u ? 2.0f * lb : la * -1.386294361f;  // -2 ln u
+    float m2;  // -2 ln u
+    if (__builtin_expect(ua >= 0xFF000000u, 0)) {  // 1 word in 256: the series, a (rarely divergent) branch
+        const float t = __uint2float_rn(0u - ua) * 0x1p-32f;               // 1 - u (exact near 1)
+        m2 = 2.0f * (t * fmaf(t, fmaf(t, 0.333333333f, 0.5f), 1.0f));     // -ln u near 1
+    } else {
+        m2 = lg2_ftz(__uint2float_rn(ua) * 0x1p-32f) * -1.386294361f;    // log2 u, u < 1
+    }
     const float rad = m2 * rsqrt_ftz(m2);
     const float y = (float)(int)((ub & 0x7FFFFFFFu) - 0x40000000u) * 1.4629180792671596e-9f;  // pi 2^-31
     const float s = sin_ftz(y);
@@ -507,7 +510,13 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, GENERAL ? 32 / FORCE_WARPS :
                 float dx, dy, dz;
                 posq_delta(a, po, pj, dx, dy, dz);
                 float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                if (r2 < CLOSE_R2) r2 = close_delta(a, b0 + il0 + o, j, dx, dy, dz);
+                if (r2 < CLOSE_R2) {  // rare: the fp64 pair vector (and the coincidence check)
+                    r2 = close_delta(a, b0 + il0 + o, j, dx, dy, dz);
+                    if (r2 == 0.f) {
+                        coincident = true;
+                        bad_tag = (uint32_t)po.w & (GENERAL && a.ns > 1 ? 0x0FFFFFFFu : 0xFFFFFFFFu);
+                    }
+                }
                 uint32_t tag_i = (uint32_t)po.w, tag_j = (uint32_t)pj.w;
                 float ca = a.a, cg = a.gamma, cs = a.sigma_dt;
                 if (GENERAL && a.ns > 1) {  // species ride in the top 4 bits of the tag word
@@ -524,10 +533,6 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, GENERAL ? 32 / FORCE_WARPS :
                 uint32_t u1 = (ifirst ? sig_j : sig_i) ^ a.step_mix;
                 tea4(u0, u1);
                 const float xi = gaussian_pair(u0, u1);
-                if (r2 == 0.f) {
-                    coincident = true;
-                    bad_tag = tag_i;
-                }
                 int qx, qy, qz;
                 pair_shares<GENERAL>(dx, dy, dz, r2, vo, vj, xi, ca, cg, cs, a.inv_rc, a.s_exp, a.smode,
                                      qx, qy, qz);
