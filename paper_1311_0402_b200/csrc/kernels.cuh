@@ -1125,7 +1125,13 @@ constexpr uint32_t RB_NONE = 0xFFFFFFFFu;
 #ifndef DPDB_RB_AHEAD
 #define DPDB_RB_AHEAD 2
 #endif
-constexpr int RB_AHEAD = DPDB_RB_AHEAD;  // walk lookahead (A/B: 2 vs 4 position loads in flight per lane)
+constexpr int RB_AHEAD = DPDB_RB_AHEAD;
+// flat-list bucket of a partner: bits [BUCKET_SHIFT, BUCKET_SHIFT + 4) of j
+// (A/B: a multiplicative hash of the line j >> 3 instead was 0.7% slower)
+#ifndef DPDB_BUCKET_SHIFT
+#define DPDB_BUCKET_SHIFT 3
+#endif
+constexpr int BUCKET_SHIFT = DPDB_BUCKET_SHIFT;  // walk lookahead (A/B: 2 vs 4 position loads in flight per lane)
 
 // Rows whose front count + cut-out length could exceed max_neighbors: the
 // exact number of in-block j < i within r_c + skin (the row's back entries),
@@ -1369,7 +1375,7 @@ __global__ void __launch_bounds__(RB_THREADS, 1024 / RB_THREADS) k_build_range(B
             // ~47 lines of 8 particles), so with the items of a line side by
             // side a 32-lane gather of the force kernel touches a few lines
             // instead of ~20 (row order) and its pair batches hold distinct
-            // owner rows.  A counting sort on a 4-bit hash of the line: each
+            // owner rows.  A counting sort on 4 bits of the line (j >> 3): each
             // lane (row) counts its own items in its column of a [bucket][lane]
             // u16 histogram (this warp's share of rl), a scan turns the counts
             // into offsets in (bucket, row) order, the items are placed in this
@@ -1384,7 +1390,7 @@ __global__ void __launch_bounds__(RB_THREADS, 1024 / RB_THREADS) k_build_range(B
             constexpr uint32_t STG = RB_SLOTS * 32;  // staging words per warp
             uint32_t* tl = a.plist + (size_t)(i & ~31u) * maxn;
             const uint32_t rowbits = lane << 26;
-            auto bucket_of = [](uint32_t e) { return (((e & 0x03FFFFFFu) >> 3) * 0x9E3779B1u) >> 28; };
+            auto bucket_of = [](uint32_t e) { return (e >> BUCKET_SHIFT) & 15u; };
             auto hist = [&](uint32_t h) -> uint16_t& { return rl[h >> 5][wbase + (h & 31u)]; };  // h = b*32 + lane
             __syncwarp();
             if (tot <= STG) {
