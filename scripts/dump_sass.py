@@ -24,6 +24,7 @@ KERNELS = {
     "integrate_final": "_ZN4dpdb11k_integrateILb1ELb0ELb0ELb0EEEvNS_13IntegrateArgsE",
     "pack_update": "_ZN4dpdb6k_packILb1EEEvNS_8PackArgsEPv",
     "unpack_update": "_ZN4dpdb8k_unpackILb1EEEvNS_10UnpackArgsEPKv",
+    "put_ghost_update": "_ZN4dpdb5k_putENS_7PutArgsE",
 }
 
 
