@@ -465,12 +465,17 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, GENERAL ? 32 / FORCE_WARPS :
     __shared__ int4 own_p[FORCE_WARPS][32];
     __shared__ float4 own_v[FORCE_WARPS][32];
     __shared__ int acc[FORCE_BLOCK * 3];
+    // GENERAL: the species-pair coefficients (a, gamma, sigma/sqrt(dt)) in
+    // shared memory -- indexed from the kernel parameters, lanes with different
+    // species pairs would serialise on the constant cache
+    __shared__ float4 coef[GENERAL ? 16 : 1];
     const uint32_t blk = blockIdx.x;
     if (a.blk_sel && a.blk_sel[blk] != a.sel_val) return;  // whole CTA
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t b0 = blk * FORCE_BLOCK;
     const uint32_t bn = min((uint32_t)FORCE_BLOCK, a.n - b0);
     for (int t = threadIdx.x; t < FORCE_BLOCK * 3; t += FORCE_WARPS * 32) acc[t] = 0;
+    if (GENERAL && threadIdx.x < 16) coef[threadIdx.x] = make_float4(a.ta[threadIdx.x], a.tg[threadIdx.x], a.ts[threadIdx.x], 0.f);
     __syncthreads();
     const uint32_t lt = lanemask_lt();
     const uint32_t maxn = MAXN ? (uint32_t)MAXN : a.maxn;
@@ -520,10 +525,10 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, GENERAL ? 32 / FORCE_WARPS :
                 uint32_t tag_i = (uint32_t)po.w, tag_j = (uint32_t)pj.w;
                 float ca = a.a, cg = a.gamma, cs = a.sigma_dt;
                 if (GENERAL && a.ns > 1) {  // species ride in the top 4 bits of the tag word
-                    const uint32_t q = (tag_i >> 28) * a.ns + (tag_j >> 28);
-                    ca = a.ta[q];
-                    cg = a.tg[q];
-                    cs = a.ts[q];
+                    const float4 cf = coef[(tag_i >> 28) * a.ns + (tag_j >> 28)];
+                    ca = cf.x;
+                    cg = cf.y;
+                    cs = cf.z;
                     tag_i &= 0x0FFFFFFFu;
                     tag_j &= 0x0FFFFFFFu;
                 }
