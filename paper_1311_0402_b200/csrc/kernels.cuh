@@ -1156,8 +1156,11 @@ __device__ __noinline__ uint32_t cut_hits(const float4* __restrict__ pos4, const
     return n;
 }
 
+#ifndef DPDB_RB_MINB
+#define DPDB_RB_MINB (1024 / DPDB_RB_THREADS)
+#endif
 template <bool WALK, bool GH>
-__global__ void __launch_bounds__(RB_THREADS, 1024 / RB_THREADS) k_build_range(BuildArgs a) {
+__global__ void __launch_bounds__(RB_THREADS, DPDB_RB_MINB) k_build_range(BuildArgs a) {
     extern __shared__ uint32_t rb_smem[];  // RB_SMEM bytes (dynamic: > 48 KB)
     uint32_t(*rs)[RB_THREADS] = reinterpret_cast<uint32_t(*)[RB_THREADS]>(rb_smem);
     uint16_t(*rl)[RB_THREADS] =
