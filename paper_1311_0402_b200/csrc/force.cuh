@@ -431,10 +431,6 @@ __global__ void __launch_bounds__(TC_WARPS * 32) k_tile_compact(const uint32_t* 
 // Each warp takes tiles (w, FORCE_TILES - 1 - w) of the block: in-block pairs are taken by
 // the lower index, so early tiles carry more pairs; pairing them with late
 // tiles evens out the work before the block's final barrier.
-#ifndef DPDB_FW_UNCOND
-#define DPDB_FW_UNCOND 0
-#endif
-constexpr bool FW_UNCOND = DPDB_FW_UNCOND;
 #ifndef FW_MINB
 // resident CTAs per SM the register allocation must allow: 40 warps / SM
 // (48 registers, 8 bytes of spill; A/B at 8 warps per CTA with the flat pair
