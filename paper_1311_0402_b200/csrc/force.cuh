@@ -412,21 +412,23 @@ __global__ void __launch_bounds__(TC_WARPS * 32) k_tile_compact(const uint32_t* 
     }
 }
 
-// Force kernel for the step pipeline's walk layout (k_build_lane<true> /
-// k_build<.., true>): same physics, pair set and fixed-point accumulation as
+// Force kernel for the step pipeline's walk layout (the range builder's
+// line-grouped flat lists; k_build_lane<true> / k_build<.., true> through
+// k_tile_compact): same physics, pair set and fixed-point accumulation as
 // k_force, restructured so the per-candidate filter (phase A) is as cheap as
-// the hardware allows -- ~27 candidates are filtered per particle but only ~8
-// pairs evaluated, so phase A dominates the instruction count.
+// the hardware allows -- ~18 front candidates are filtered per particle but
+// only ~8 pairs evaluated.
 //
-// Phase A (per candidate, per lane = row): one row-entry load and one posq
-// load, fp32 distance, |r| <= r_c, a ballot, and one 4-byte shared store of
-// j | lane << 27 into the warp's pair queue.  Everything else the pair needs
-// (d, tags, in-block test) is recomputed in phase B, which runs
-// with all 32 lanes busy.  Row entries are fetched one group of 4 ahead with
-// compile-time strides (MAXN) and the 4 candidate positions of a group are
-// issued back to back, so each warp keeps up to 8 loads in flight without a
-// rotating register pipeline.  The queue (160 slots) is drained once per
-// group, in whole batches of 32.
+// Phase A (one flat-list item per lane, 32 items per step, every lane busy):
+// the list word and the partner's posq, fp32 distance, |r| <= r_c, a ballot,
+// and one 4-byte shared store of the item (j | row << 26 | skin << 31) into
+// the warp's pair queue.  Everything else the pair needs (d, tags, in-block
+// test) is recomputed in phase B, which runs with all 32 lanes busy.  A group
+// is 4 steps: its 4 partner gathers are issued back to back and the next
+// group's list words prefetched, so each warp keeps up to 8 loads in flight.
+// With the range builder's line-grouped lists the 32 gathers of a step touch a
+// few cache lines and a queued batch holds several owner rows.  The queue
+// (160 slots) is drained once per group, in whole batches of 32.
 //
 // Each warp takes tiles (w, FORCE_TILES - 1 - w) of the block: in-block pairs are taken by
 // the lower index, so early tiles carry more pairs; pairing them with late
