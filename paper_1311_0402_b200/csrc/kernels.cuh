@@ -1094,11 +1094,12 @@ __global__ void __launch_bounds__(256) k_build_lane(BuildArgs a) {
 // GH: the context has ghost rows (a brick); only then is each hit tested for a
 //     ghost partner (the block's blk_ghost flag).
 //  WALK: only the entries the force kernel evaluates (j outside the block or
-//        j > i) -- the row's "front" entries -- go to the tile's flat pair
-//        list (the force kernel's input): at each walk step the lanes with a
-//        hit append j | row << 26 | skin << 31 at the list tail +
-//        popc(ballot & lanemask_lt), so every row's entries stay in ascending
-//        order inside the list; fwalk = n_front | flags.  The in-block j < i
+//        j > i) -- the row's "front" entries -- are kept: the walk stores them
+//        in the row's tile-transposed scratch row, then the warp writes the
+//        tile's flat pair list (the force kernel's input) as items
+//        j | row << 26 | skin << 31 grouped by the partner's cache line (a
+//        counting sort on bits 3-6 of j; each row's items stay ascending
+//        within a group); fwalk = n_front | flags.  The in-block j < i
 //        entries are not stored -- they are exactly the transposes of the
 //        block's front entries (unwalk restores them).  No atomics: the full
 //        row length n_front + n_back is bounded by n_front + the length of the
