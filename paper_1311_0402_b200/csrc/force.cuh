@@ -453,7 +453,11 @@ constexpr bool FW_PREFETCH = DPDB_FW_PREFETCH;  // A/B switch: L1 prefetch of ve
 #define DPDB_FW_IL 1
 #endif
 constexpr int FW_IL = DPDB_FW_IL;
-constexpr int FW_Q = 32 * FW_IL + 128;  // < 32 FW_IL leftovers + 4 x 32 hits per group
+#ifndef DPDB_FW_G
+#define DPDB_FW_G 4
+#endif
+constexpr int FW_G = DPDB_FW_G;  // phase-A steps (of 32 items) per group: gathers in flight per lane
+constexpr int FW_Q = 32 * FW_IL + 32 * FW_G;  // < 32 FW_IL leftovers + FW_G x 32 hits per group
 
 template <bool GENERAL, bool BODY, int MAXN, int FUSE>
 __global__ void __launch_bounds__(FORCE_WARPS * 32, GENERAL ? 32 / FORCE_WARPS : FW_MINB)
@@ -564,17 +568,17 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, GENERAL ? 32 / FORCE_WARPS :
         const char* vb = reinterpret_cast<const char*>(a.vel4);
         uint32_t* qw = q_j[warp];
         const float rc2 = a.rc2;
-        auto group = [&](uint32_t c0, const uint32_t (&cur)[4], uint32_t (&nxt)[4]) {
-            int4 p[4];
+        auto group = [&](uint32_t c0, const uint32_t (&cur)[FW_G], uint32_t (&nxt)[FW_G]) {
+            int4 p[FW_G];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < FW_G; ++k) {
                 const uint32_t jk = c0 + 32u * k + lane < cnt ? (cur[k] & 0x03FFFFFFu) : b0;
                 p[k] = __ldg(reinterpret_cast<const int4*>(pb + ((size_t)jk << 4)));
             }
 #pragma unroll
-            for (int k = 0; k < 4; ++k) nxt[k] = __ldg(pl + c0 + 128u + 32u * k);  // coalesced
+            for (int k = 0; k < FW_G; ++k) nxt[k] = __ldg(pl + c0 + 32u * FW_G + 32u * k);  // coalesced
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < FW_G; ++k) {
                 const int4 po = own_p[warp][(cur[k] >> 26) & 31u];
                 float dx, dy, dz;
                 posq_delta(a, po, p[k], dx, dy, dz);
@@ -614,14 +618,14 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, GENERAL ? 32 / FORCE_WARPS :
                 qtail = left;
             }
         };
-        uint32_t ea[4], eb[4];
+        uint32_t ea[FW_G], eb[FW_G];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) ea[k] = __ldg(pl + 32u * k);
+        for (int k = 0; k < FW_G; ++k) ea[k] = __ldg(pl + 32u * k);
 #pragma unroll 1
-        for (uint32_t c0 = 0; c0 < cnt; c0 += 256) {
+        for (uint32_t c0 = 0; c0 < cnt; c0 += 64u * FW_G) {
             group(c0, ea, eb);
-            if (c0 + 128 >= cnt) break;
-            group(c0 + 128, eb, ea);
+            if (c0 + 32u * FW_G >= cnt) break;
+            group(c0 + 32u * FW_G, eb, ea);
         }
         __syncwarp();
         if (qtail > 0) {  // the rest, interleaved the same way
