@@ -481,8 +481,6 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, GENERAL ? 32 / FORCE_WARPS :
     __syncthreads();
     const uint32_t lt = lanemask_lt();
     const uint32_t maxn = MAXN ? (uint32_t)MAXN : a.maxn;
-    bool coincident = false;
-    uint32_t bad_tag = 0;
 
 #pragma unroll 1
     for (int pass = 0; pass < FORCE_TPW; ++pass) {
@@ -519,10 +517,9 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, GENERAL ? 32 / FORCE_WARPS :
                 float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
                 if (r2 < CLOSE_R2) {  // rare: the fp64 pair vector (and the coincidence check)
                     r2 = close_delta(a, b0 + il0 + o, j, dx, dy, dz);
-                    if (r2 == 0.f) {
-                        coincident = true;
-                        bad_tag = (uint32_t)po.w & (GENERAL && a.ns > 1 ? 0x0FFFFFFFu : 0xFFFFFFFFu);
-                    }
+                    if (r2 == 0.f)  // raised on the spot: no flag held live through the loop
+                        raise_err(a.err, DPDB_EPHYSICS, EW_COINCIDENT,
+                                  (uint32_t)po.w & (GENERAL && a.ns > 1 ? 0x0FFFFFFFu : 0xFFFFFFFFu), 0u);
                 }
                 uint32_t tag_i = (uint32_t)po.w, tag_j = (uint32_t)pj.w;
                 float ca = a.a, cg = a.gamma, cs = a.sigma_dt;
@@ -637,7 +634,6 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, GENERAL ? 32 / FORCE_WARPS :
         }
         __syncwarp();
     }
-    if (coincident) raise_err(a.err, DPDB_EPHYSICS, EW_COINCIDENT, bad_tag, 0u);
     // FUSE: fetch the block's fp64 x, v and tags for the Verlet epilogue before
     // the barrier, so the loads overlap the wait for the block's last warps
     constexpr int PER_T = FORCE_BLOCK / (FORCE_WARPS * 32);
