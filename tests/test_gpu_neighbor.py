@@ -128,6 +128,35 @@ def test_pipeline_walk_layout_exports_reference_rows():
     assert np.array_equal(f_walk, f_joined)
 
 
+@pytest.mark.parametrize("rho", [3.0, 6.5])
+def test_pipeline_walk_layout_dense_tiles(rho, monkeypatch):
+    """At rho 6.5 a tile's flat list (~1,200 items) exceeds the range
+    builder's shared-memory staging (928 words), so the builder falls back to
+    row order for those tiles; rows still export exactly, and the run equals
+    the all-row-order one (DPDB_BUCKET=0) bit for bit."""
+    maxn = 128
+    box, obox, st = _sys.fluid((9.5, 9.5, 9.5), rho, seed=13)
+    E, core, skin, s = oracle_table(obox, st, maxn)
+    out = []
+    for b in ("1", "0"):
+        monkeypatch.setenv("DPDB_BUCKET", b)
+        e = _sys.engine(box, st)
+        e.setup()
+        t = e.neighbor_table()
+        assert np.array_equal(t.core_count, core[: t.n_rows]) and np.array_equal(t.skin_count, skin[: t.n_rows])
+        for i in range(t.n_rows):
+            assert np.array_equal(t.core_row(i), E[i, : core[i]])
+            assert np.array_equal(t.skin_row(i), E[i, maxn - skin[i]:][::-1])
+        e.close()
+        e = _sys.engine(box, st)
+        e.setup()
+        e.step(12)
+        out.append(e.download())
+        e.close()
+    for u, w in zip(out[0].coord + out[0].veloc + out[0].force, out[1].coord + out[1].veloc + out[1].force):
+        assert np.array_equal(u, w)
+
+
 def test_overflow_is_physics_error():
     box, obox, st = _sys.fluid((4.0, 4.0, 4.0), 50, seed=3)
     e = _sys.engine(box, st, run=dpd.RunConfig(max_neighbors=128))
